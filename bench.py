@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""Benchmark of the COMET W4Ax hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl comet|reference] [--config NAME]
+
+Workload (default, BASELINE.json configs[1]): LLaMA-2-7B linear shapes,
+K=4096, N in {4096, 11008}, M=4096 tokens (the top of the M=1..4096 range),
+3/32 INT8 blocks (~10%), group-128 INT4 weights, seeded synthetic inputs
+(paper_2410_12168_b200.synth).  One step = one pass of the hot path over
+both layers: quantize_act (a1+a2) + w4ax_gemm (a3..a8) per layer
+(+ the NCCL all-gather of Y when N>1: weights N-sharded, X replicated).
+Weights are packed once before timing (a0 is offline); its time is
+reported separately as pack_weight_ms.
+
+Timing: W untimed warm-up steps, then K steps; L2 is flushed (256 MiB
+write) before every timed step outside the timed events; each step is
+timed with CUDA events on the launching stream and summed; barrier +
+synchronize on both sides; max over ranks.  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "W4Ax GEMM TOPS & % of B200 INT8/HBM roofline; linear-layer tokens/s at 1/2/4/8 GPU"
+
+CONFIGS = {
+    # BASELINE.json configs[1]
+    "llama2-7b": dict(workload="LLaMA-2-7B linear shapes (K=4096, N=4096/11008), M=4096, 3/32 INT8 blocks, g=128",
+                      M=4096, layers=[(4096, 4096), (11008, 4096)], n8=[3, 3]),
+    # decode point of the same config
+    "llama2-7b-decode": dict(workload="LLaMA-2-7B linear shapes (K=4096, N=4096/11008), M=16 decode, 3/32 INT8 blocks",
+                             M=16, layers=[(4096, 4096), (11008, 4096)], n8=[3, 3]),
+    # BASELINE.json configs[3] (single-GPU share of the 70B prefill)
+    "llama3-70b": dict(workload="LLaMA-3-70B gate_up (57344x8192) + down (8192x28672), M=8192, 6/64 + 22/224 INT8",
+                       M=8192, layers=[(57344, 8192), (8192, 28672)], n8=[6, 22]),
+    "llama3-70b-decode": dict(workload="LLaMA-3-70B gate_up + down, M=16 decode", M=16,
+                              layers=[(57344, 8192), (8192, 28672)], n8=[6, 22]),
+    # BASELINE.json configs[0]
+    "tiny": dict(workload="tiny W4Ax GEMM M=16 N=256 K=512, one INT8 block", M=16, layers=[(256, 512)], n8=[1]),
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return {"hbm_gbs": pk["hbm_gbs"], "bf16_tflops": pk["bf16_tflops"],
+                "bf16_tflops_sustained": pk.get("bf16_tflops_sustained"), "src": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "src": "fallback"}
+
+
+def load_traffic(config_name):
+    """dram bytes per GEMM launch from a committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(config_name)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------ clocks ----
+class ClockSampler:
+    def __init__(self, dev_index=0, period=0.05):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period, self._stop = period, threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    REASONS = {0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x4: "sw_power_cap", 0x1: "gpu_idle"}
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------ distributed ----
+def dist_setup(ngpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        rank, local = int(os.environ["RANK"]), int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return rank, world, local
+    return 0, 1, 0
+
+
+def shard_rows(N, world, rank, align=128):
+    """Column-parallel shard [n0, n1) of the N output channels (multiples of 128, equal padded width)."""
+    per = -(-N // world)
+    per = -(-per // align) * align
+    n0 = min(rank * per, N)
+    return n0, min(n0 + per, N), per
+
+
+# ---------------------------------------------------------- reference ----
+def run_reference(args, cfg):
+    """--impl reference: the CPU oracle as it stands on the host cores."""
+    import oracle
+    from paper_2410_12168_b200 import synth
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    M = cfg["M"]
+    rows = synth.sample_rows(M, 4 if M > 4 else M, seed=1)
+    layers = []
+    for li, ((N, K), n8) in enumerate(zip(cfg["layers"], cfg["n8"])):
+        p = synth.make_problem(M, N, K, n8=n8, seed=100 + li, x_rows=rows)
+        Wq, Sw = oracle.pack_weight(p["W"], 128, p["perm"])
+        layers.append((p, Wq, Sw))
+
+    def step():
+        for p, Wq, Sw in layers:
+            Xq8, Xq4, Sx = oracle.quantize_act(p["X"], p["bits"], p["perm"])
+            oracle.w4ax_gemm(Xq8, Xq4, Sx, p["bits"], Wq, Sw, group=128)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    ops = sum(2.0 * len(rows) * N * K for (N, K) in cfg["layers"])
+    tops = ops / dt / 1e12
+    cores = oracle.num_threads()
+    sample = f"{len(rows)} of {M} token rows per layer (quantize+GEMM+dequant, pre-packed weights)"
+    out = {"impl": "reference", "metric": METRIC, "value": tops, "unit": "TOPS", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "int8/int32+f64", "data": "synthetic",
+           "config": {"workload": cfg["workload"], "M": M, "layers": cfg["layers"]},
+           "tokens_per_s": len(rows) / dt,
+           "cpu_baseline": {"value": tops, "unit": "TOPS", "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": tops, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+def cpu_baseline(cfg, seconds_target=10.0):
+    """Oracle timed on the host cores on a bounded row sample (rank 0, N=1)."""
+    import oracle
+    from paper_2410_12168_b200 import synth
+    M = cfg["M"]
+    nrows = 8 if M >= 8 else M
+    rows = synth.sample_rows(M, nrows, seed=2)
+    layers = []
+    for li, ((N, K), n8) in enumerate(zip(cfg["layers"], cfg["n8"])):
+        p = synth.make_problem(M, N, K, n8=n8, seed=100 + li, x_rows=rows)
+        Wq, Sw = oracle.pack_weight(p["W"], 128, p["perm"])
+        layers.append((p, Wq, Sw))
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        for p, Wq, Sw in layers:
+            Xq8, Xq4, Sx = oracle.quantize_act(p["X"], p["bits"], p["perm"])
+            oracle.w4ax_gemm(Xq8, Xq4, Sx, p["bits"], Wq, Sw, group=128)
+        reps += 1
+        if time.perf_counter() - t0 > seconds_target or reps >= 50:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    ops = sum(2.0 * len(rows) * N * K for (N, K) in cfg["layers"])
+    return {"value": ops / dt / 1e12, "unit": "TOPS", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{len(rows)} of {M} token rows x {len(layers)} layers, {reps} reps "
+                      f"(quantize + per-block INT32 GEMM + fp64 dequant; weights pre-packed)",
+            "tokens_per_s": len(rows) / dt}
+
+
+# -------------------------------------------------------------- comet ----
+def run_comet(args, cfg, config_name):
+    import torch
+    import torch.distributed as dist
+    from paper_2410_12168_b200 import comet, synth
+
+    rank, world, local = dist_setup(args.gpus)
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    M = cfg["M"]
+    stream = torch.cuda.current_stream()
+
+    layers = []
+    t_pack = 0.0
+    for li, ((N, K), n8) in enumerate(zip(cfg["layers"], cfg["n8"])):
+        p = synth.make_problem(M, N, K, n8=n8, seed=100 + li)
+        n0, n1, per = shard_rows(N, world, rank)
+        Wl = np.zeros((per, K), np.float16)
+        Wl[: n1 - n0] = p["W"][n0:n1]
+        W = torch.from_numpy(Wl).to(dev)
+        perm = torch.from_numpy(p["perm"]).to(dev)
+        bits = comet.BlockBits(p["bits"])
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        Wq, Sw = comet.comet_pack_weight(W, perm, 128)
+        e1.record()
+        torch.cuda.synchronize()
+        t_pack += e0.elapsed_time(e1)
+        X = torch.from_numpy(p["X"]).to(dev)
+        planes = comet.alloc_act_planes(M, K, bits, dev)
+        Y = torch.empty((M, per), dtype=torch.float16, device=dev)
+        ws = comet.new_workspace(comet.comet_w4ax_gemm_workspace_bytes(M, per, K), dev)
+        Yall = torch.empty((world, M, per), dtype=torch.float16, device=dev) if world > 1 else None
+        Xh = torch.from_numpy(p["X"]).pin_memory()
+        Yh = torch.empty((M, per), dtype=torch.float16).pin_memory()
+        scratch = comet.new_workspace(comet.comet_w4ax_linear_scratch_bytes(M, per, K, bits), dev)
+        layers.append(dict(N=N, K=K, per=per, W=W, perm=perm, bits=bits, Wq=Wq, Sw=Sw, X=X, planes=planes, Y=Y,
+                           ws=ws, Yall=Yall, Xh=Xh, Yh=Yh, scratch=scratch, ev=[]))
+        del p
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def step(timed_kernels=False):
+        for L in layers:
+            Xq8, Xq4, Sx = comet.comet_quantize_act(L["X"], L["bits"], L["perm"], out=L["planes"])
+            if timed_kernels:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+            comet.comet_w4ax_gemm(Xq8, Xq4, Sx, L["bits"], L["Wq"], L["Sw"], 128, out=L["Y"], workspace=L["ws"])
+            if timed_kernels:
+                b.record(stream)
+                L["ev"].append((a, b))
+            if world > 1:
+                dist.all_gather_into_tensor(L["Yall"], L["Y"])
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3) if args.warmup >= 3 else 3):
+        step()
+    barrier()
+
+    # ---- device-timed region ----
+    n_launch0 = comet.launch_count()
+    step_ms = []
+    with ClockSampler(local) as clk:
+        barrier()
+        for _ in range(args.steps):
+            flush.fill_(1)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            step(timed_kernels=True)
+            s1.record(stream)
+            step_ms.append((s0, s1))
+        barrier()
+    launches = comet.launch_count() - n_launch0
+    t_dev = sum(a.elapsed_time(b) for a, b in step_ms) / args.steps  # ms per step
+    gemm_ms = [sum(a.elapsed_time(b) for a, b in L["ev"]) / len(L["ev"]) for L in layers]
+    L0 = layers[0]
+
+    # ---- end-to-end through the C ABI with host buffers ----
+    barrier()
+    e2e_ms = []
+    for it in range(args.warmup + args.steps):
+        barrier()
+        t0 = time.perf_counter()
+        for L in layers:
+            comet.comet_w4ax_linear(L["Xh"], L["bits"], L["Wq"], L["Sw"], perm=L["perm"], out=L["Yh"],
+                                    scratch=L["scratch"])
+        torch.cuda.synchronize()
+        if it >= args.warmup:
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_t = statistics.median(e2e_ms)
+
+    if world > 1:
+        t = torch.tensor([t_dev, e2e_t] + gemm_ms, dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_dev, e2e_t, gemm_ms = float(t[0]), float(t[1]), [float(v) for v in t[2:]]
+
+    ops = sum(2.0 * M * L["N"] * L["K"] for L in layers)
+    tops = ops / (t_dev * 1e-3) / 1e12
+    e2e_tops = ops / (e2e_t * 1e-3) / 1e12
+    h2d = sum(M * L["K"] * 2 for L in layers)
+    d2h = sum(M * L["per"] * 2 for L in layers)
+
+    # roofline of the dominant kernel (the GEMM of the largest layer)
+    peaks = load_peaks()
+    dom = int(np.argmax(gemm_ms))
+    Ld = layers[dom]
+    ops_d = 2.0 * M * Ld["per"] * Ld["K"]
+    nb = Ld["K"] // 128
+    n8 = Ld["bits"].n8
+    bytes_d = (Ld["per"] * Ld["K"] / 2 + 4 * Ld["per"] * nb + M * (128 * n8 + 64 * (nb - n8)) + 4 * M * nb
+               + 2 * M * Ld["per"])
+    int8_peak = 2.0 * peaks["bf16_tflops"]  # dense int8 = 2x bf16 (nominal 4.5 vs 2.25 PF)
+    t_tc = ops_d / (int8_peak * 1e12)
+    t_hbm = bytes_d / (peaks["hbm_gbs"] * 1e9)
+    if t_tc >= t_hbm:
+        achieved = ops_d / (gemm_ms[dom] * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TOPS",
+                "peak_src": f"{peaks['src']} bf16 burst x2 (int8 = 2x bf16 dense)"}
+    else:
+        achieved = bytes_d / (gemm_ms[dom] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "peak_src": f"{peaks['src']} copy bandwidth"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    tr = load_traffic(config_name)
+    roof["traffic"] = tr.get(f"layer{dom}") if isinstance(tr, dict) else None
+    roof["kernel"] = f"w4ax_gemm layer{dom} (N={Ld['per']}, K={Ld['K']}), {gemm_ms[dom] * 1e3:.1f} us/launch"
+
+    out = {"metric": METRIC, "value": tops, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": t_dev, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "int8 (INT4/INT8 operands) x int32 accum, fp32 dequant, fp16 out",
+           "data": "synthetic (seeded; X~N(0,1) + planted outlier channels, W~N(0,1/K))",
+           "config": {"workload": cfg["workload"], "M": M, "layers": cfg["layers"], "group": 128,
+                      "parallelism": f"tp{world} (N-sharded, NCCL all-gather of Y)" if world > 1 else "single GPU",
+                      "l2": "flushed (256 MiB write) before every timed step, outside the events"},
+           "tokens_per_s": M / (t_dev * 1e-3),
+           "gemm_us": [g * 1e3 for g in gemm_ms],
+           "pack_weight_ms": t_pack,
+           "e2e": {"value": e2e_tops, "unit": "TOPS", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                   "ms_per_step": e2e_t, "api": "comet_w4ax_linear (host pinned X in, host Y out)"},
+           "gpu_launches": launches,
+           "roofline": roof,
+           "clocks": clk.summary()}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg, seconds_target=args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="comet", choices=["comet", "reference"])
+    ap.add_argument("--config", default="llama2-7b", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_comet(args, cfg, args.config)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

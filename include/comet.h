@@ -1,0 +1,143 @@
+/*
+ * comet.h -- C ABI of libcomet.so, the B200 (sm_100a) implementation of
+ * COMET's W4Ax mixed-precision GEMM (arXiv 2410.12168; PAPER.md cited as
+ * P:L<line> §<section>).
+ *
+ * The paper's problem statement is the linear layer O = WX with 4-bit
+ * weights and FMPQ activations (§5): activations are split along the
+ * channel axis into blocks of k = 128 channels (§3.2); outlier
+ * channels are clustered by a channel permutation into a few blocks
+ * (§3.2) which are quantized to INT8, all other blocks to INT4; the
+ * weight reduction axis is permuted identically.  The kernel is
+ * "a standalone .so dynamic library" with "a set of C++ APIs"; this
+ * header is that API as plain C.
+ *
+ * Conventions (all entry points):
+ *   - Tensor pointers are DEVICE pointers owned by the caller unless stated
+ *     otherwise; nothing here allocates, frees or synchronizes.  Work is
+ *     enqueued on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *   - Every argument is validated on the host before any launch; a call that
+ *     returns an error has no side effects.
+ *   - block size is fixed at COMET_BLOCK = 128 channels; K % 128 == 0.
+ *   - `block_bits` is a HOST array of K/128 entries, each 4 or 8 (the static
+ *     per-layer precision mask from calibration); the same array and
+ *     the same `perm` must be given to comet_pack_weight/comet_quantize_act
+ *     and comet_w4ax_gemm of one layer.
+ *   - `perm` is a DEVICE int32[K] with perm[new] = old (a bijection on
+ *     [0,K)), or NULL for the identity.
+ *   - Inputs must be finite; non-finite input gives unspecified output.
+ *   - Results are deterministic (same inputs, shape and device -> identical
+ *     bits); no floating-point atomics are used.
+ *
+ * Data layouts (row-major; "bytes" are leading dimensions in bytes):
+ *   X   fp16 [M x K], row stride ldx elements (ldx >= K, ldx % 8 == 0).
+ *   Xq8 int8 [M x K8], K8 = 128 * #INT8 blocks; INT8 block b occupies
+ *       columns [128*r8(b), 128*r8(b)+128) where r8(b) = number of INT8
+ *       blocks before b.
+ *   Xq4 packed INT4 [M x K4/2 bytes], K4 = 128 * #INT4 blocks; INT4 block b
+ *       occupies bytes [64*r4(b), 64*r4(b)+64).  Nibble order: every 8
+ *       consecutive elements e0..e7 form one little-endian 32-bit word whose
+ *       byte j = (e_j & 0xF) | (e_{j+4} & 0xF) << 4 -- the 32-bit form of the
+ *       paper's W1<->W2 "location switch" (§4.3), so that
+ *       (w << 4) & 0xF0F0F0F0 and w & 0xF0F0F0F0 are 16*e0..3 and 16*e4..7
+ *       as int8 ("zero extension ... multiplied by 16").
+ *   Sx  fp32 [K/128 x ldsx], Sx[b*ldsx + m] = scale of row m, block b;
+ *       ldsx >= M, ldsx % 4 == 0; entries m in [M, ldsx) are written as 1.0.
+ *   Wq  packed INT4 [N x K/2 bytes], same nibble order, K on the permuted axis.
+ *   Sw  fp32 [K/group x N], Sw[j*N + n] = scale of output channel n, group j.
+ *   Y   fp16 [M x N], row stride ldy elements (ldy >= N, ldy % 8 == 0).
+ * Quantization (all blocks, weights and activations): symmetric absmax,
+ * a = max|x|, s = a/qmax, r = qmax/a (IEEE fp32), q = round_half_away(x*r),
+ * qmax = 7 (INT4) or 127 (INT8); an all-zero block has s = 1, q = 0.
+ */
+#ifndef COMET_H_
+#define COMET_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define COMET_BLOCK 128
+
+typedef enum {
+  COMET_OK = 0,
+  COMET_ERR_INVALID_ARG = 1, /* NULL where required, M/N/K < 0, bad block_bits entry */
+  COMET_ERR_SHAPE = 2,       /* K%128, N%128, group not in {128, K}, ld too small, K > 65536 */
+  COMET_ERR_ALIGNMENT = 3,   /* pointer or leading dimension not 16-byte aligned */
+  COMET_ERR_WORKSPACE = 4,   /* workspace/scratch smaller than the size query returns */
+  COMET_ERR_UNSUPPORTED = 5, /* device is not sm_100 (B200) */
+  COMET_ERR_CUDA = 6         /* CUDA launch/runtime error (comet_last_cuda_error()) */
+} comet_status;
+
+typedef void* comet_stream_t; /* cudaStream_t */
+
+/* ---- size helpers (host, pure; -1 on invalid arguments) ---------------- */
+int64_t comet_act_plane8_bytes(int32_t M, int32_t K, const uint8_t* block_bits); /* M*K8   */
+int64_t comet_act_plane4_bytes(int32_t M, int32_t K, const uint8_t* block_bits); /* M*K4/2 */
+int64_t comet_act_ldsx(int32_t M);                                               /* roundup(M,4) */
+/* device workspace comet_w4ax_gemm needs for split-K partials + tile counters */
+int64_t comet_w4ax_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K);
+/* device scratch comet_w4ax_linear needs (planes + scales + gemm workspace) */
+int64_t comet_w4ax_linear_scratch_bytes(int32_t M, int32_t N, int32_t K, const uint8_t* block_bits);
+
+/* ---- a0: offline weight preparation -------------------
+ * W fp16 [N x K] (row stride ldw) -> Wq packed INT4 [N x K/2], Sw fp32
+ * [K/group x N].  The K axis is permuted by `perm` first (weights are
+ * permuted like the activations), then quantized per (n, group of
+ * `group` consecutive permuted channels), group in {128, K}. */
+comet_status comet_pack_weight(const void* W, int64_t ldw, int32_t N, int32_t K, const int32_t* perm,
+                               int32_t group, void* Wq, float* Sw, comet_stream_t stream);
+
+/* ---- a1+a2: FMPQ activation quantization --------------
+ * X fp16 [M x K] -> Xq8, Xq4, Sx (layouts above).  The channel permutation
+ * is fused (gather) into the quantizer.  Xq8 may be NULL iff K8 == 0 and
+ * Xq4 may be NULL iff K4 == 0.  M == 0 is a no-op. */
+comet_status comet_quantize_act(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
+                                const uint8_t* block_bits, int8_t* Xq8, void* Xq4, float* Sx, int64_t ldsx,
+                                comet_stream_t stream);
+
+/* ---- a3..a8: the W4Ax GEMM -------------------------
+ * Y[m,n] = sum_b Sx[b,m] * Sw[g(b),n] * sum_{i in block b} xq[m,i]*wq[n,i]
+ * with the integer block sums exact (INT32) and the scale applied per block
+ * in fp32 ("divide by 16 in the scaling parameter"), rounded once to
+ * fp16.  N % 128 == 0.  workspace: device memory of at least
+ * comet_w4ax_gemm_workspace_bytes(M, N, K) bytes whose first 64 KiB must be
+ * zero on the first use (the kernel leaves it zero again); it may be NULL
+ * only if that size is 0. */
+comet_status comet_w4ax_gemm(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
+                             const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq, const float* Sw,
+                             int32_t N, int32_t group, void* Y, int64_t ldy, void* workspace,
+                             size_t workspace_bytes, comet_stream_t stream);
+
+/* ---- test/debug: per-block INT32 accumulators ---------------------------
+ * Acc int32 [K/128 x M x N]: Acc[(b*M + m)*N + n] = sum_{i in block b}
+ * xq[m,i]*wq[n,i] in LOGICAL units (the x16 / x256 zero-extension factors
+ * removed), computed by the same tcgen05 pipeline as comet_w4ax_gemm. */
+comet_status comet_w4ax_gemm_acc_i32(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
+                                     const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq,
+                                     const float* Sw, int32_t N, int32_t group, int32_t* Acc,
+                                     comet_stream_t stream);
+
+/* ---- the whole linear layer (user call): quantize_act + w4ax_gemm ------
+ * X and Y may be HOST (pinned or pageable) or DEVICE pointers; host buffers
+ * are copied in/out on `stream` inside the call (X: M*ldx*2 bytes in, Y:
+ * M*ldy*2 bytes out).  scratch: device memory of at least
+ * comet_w4ax_linear_scratch_bytes(M, N, K, block_bits) bytes, first 64 KiB
+ * zero on first use.  When Y is a host pointer the call synchronizes
+ * `stream` before returning. */
+comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
+                               const uint8_t* block_bits, const void* Wq, const float* Sw, int32_t N, int32_t group,
+                               void* Y, int64_t ldy, void* scratch, size_t scratch_bytes, comet_stream_t stream);
+
+const char* comet_status_str(comet_status s);
+const char* comet_last_cuda_error(void);
+/* number of kernel launches this library issued since load (host counter) */
+int64_t comet_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COMET_H_ */

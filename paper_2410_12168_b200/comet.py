@@ -1,0 +1,235 @@
+"""Python binding of libcomet.so (include/comet.h) -- argument marshalling only.
+
+Every function here has the name of the C entry point it wraps and does no
+arithmetic of the method: it checks dtypes/devices, allocates outputs with
+torch (device memory is PyTorch's job), passes raw pointers and the current
+CUDA stream, and raises on a non-OK status.  There is no CPU fallback: if
+libcomet.so is missing or the device is not sm_100, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcomet.so")
+BLOCK = 128
+
+STATUS = {0: "COMET_OK", 1: "COMET_ERR_INVALID_ARG", 2: "COMET_ERR_SHAPE", 3: "COMET_ERR_ALIGNMENT",
+          4: "COMET_ERR_WORKSPACE", 5: "COMET_ERR_UNSUPPORTED", 6: "COMET_ERR_CUDA"}
+EXPORTS = ["comet_act_plane8_bytes", "comet_act_plane4_bytes", "comet_act_ldsx", "comet_w4ax_gemm_workspace_bytes",
+           "comet_w4ax_linear_scratch_bytes", "comet_pack_weight", "comet_quantize_act", "comet_w4ax_gemm",
+           "comet_w4ax_gemm_acc_i32", "comet_w4ax_linear", "comet_status_str", "comet_last_cuda_error",
+           "comet_launch_count"]
+
+
+class CometError(RuntimeError):
+    def __init__(self, fn, status):
+        msg = f"{fn} -> {STATUS.get(status, status)}"
+        if status == 6:
+            msg += f" ({lib().comet_last_cuda_error().decode()})"
+        super().__init__(msg)
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load libcomet.so (building it first if the sources are newer)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            from . import build as _build
+            _build.build()
+        L = ctypes.CDLL(LIB_PATH)
+        P, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+        L.comet_act_plane8_bytes.argtypes = [i32, i32, P]
+        L.comet_act_plane8_bytes.restype = i64
+        L.comet_act_plane4_bytes.argtypes = [i32, i32, P]
+        L.comet_act_plane4_bytes.restype = i64
+        L.comet_act_ldsx.argtypes = [i32]
+        L.comet_act_ldsx.restype = i64
+        L.comet_w4ax_gemm_workspace_bytes.argtypes = [i32, i32, i32]
+        L.comet_w4ax_gemm_workspace_bytes.restype = i64
+        L.comet_w4ax_linear_scratch_bytes.argtypes = [i32, i32, i32, P]
+        L.comet_w4ax_linear_scratch_bytes.restype = i64
+        L.comet_pack_weight.argtypes = [P, i64, i32, i32, P, i32, P, P, P]
+        L.comet_pack_weight.restype = ctypes.c_int
+        L.comet_quantize_act.argtypes = [P, i64, i32, i32, P, P, P, P, P, i64, P]
+        L.comet_quantize_act.restype = ctypes.c_int
+        L.comet_w4ax_gemm.argtypes = [P, P, P, i64, P, i32, i32, P, P, i32, i32, P, i64, P, sz, P]
+        L.comet_w4ax_gemm.restype = ctypes.c_int
+        L.comet_w4ax_gemm_acc_i32.argtypes = [P, P, P, i64, P, i32, i32, P, P, i32, i32, P, P]
+        L.comet_w4ax_gemm_acc_i32.restype = ctypes.c_int
+        L.comet_w4ax_linear.argtypes = [P, i64, i32, i32, P, P, P, P, i32, i32, P, i64, P, sz, P]
+        L.comet_w4ax_linear.restype = ctypes.c_int
+        L.comet_status_str.argtypes = [ctypes.c_int]
+        L.comet_status_str.restype = ctypes.c_char_p
+        L.comet_last_cuda_error.argtypes = []
+        L.comet_last_cuda_error.restype = ctypes.c_char_p
+        L.comet_launch_count.argtypes = []
+        L.comet_launch_count.restype = i64
+        _lib = L
+    return _lib
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check(fn, st):
+    if st != 0:
+        raise CometError(fn, st)
+
+
+class BlockBits:
+    """Host copy of a layer's static precision mask (K/128 entries of 4/8)."""
+
+    def __init__(self, bits: Sequence[int]):
+        self.array = np.ascontiguousarray(np.asarray(bits, dtype=np.uint8))
+        self.ptr = self.array.ctypes.data_as(ctypes.c_void_p)
+        self.n8 = int((self.array == 8).sum())
+        self.n4 = int((self.array == 4).sum())
+
+    def __len__(self):
+        return self.array.size
+
+
+def as_bits(bits) -> BlockBits:
+    return bits if isinstance(bits, BlockBits) else BlockBits(bits)
+
+
+def launch_count() -> int:
+    return int(lib().comet_launch_count())
+
+
+# ----------------------------------------------------------------- sizes ----
+def comet_act_ldsx(M: int) -> int:
+    return int(lib().comet_act_ldsx(M))
+
+
+def comet_w4ax_gemm_workspace_bytes(M: int, N: int, K: int) -> int:
+    return int(lib().comet_w4ax_gemm_workspace_bytes(M, N, K))
+
+
+def comet_w4ax_linear_scratch_bytes(M: int, N: int, K: int, bits) -> int:
+    return int(lib().comet_w4ax_linear_scratch_bytes(M, N, K, as_bits(bits).ptr))
+
+
+def new_workspace(nbytes: int, device) -> Optional[torch.Tensor]:
+    """Device workspace; the first 64 KiB (tile counters) must start zeroed."""
+    if nbytes <= 0:
+        return None
+    return torch.zeros(nbytes, dtype=torch.uint8, device=device)
+
+
+# -------------------------------------------------------------- entries ----
+def comet_pack_weight(W: torch.Tensor, perm: Optional[torch.Tensor] = None, group: int = BLOCK, stream=None):
+    """a0: W fp16 [N x K] -> (Wq uint8 [N x K/2], Sw fp32 [K/group x N])."""
+    assert W.is_cuda and W.dtype == torch.float16 and W.dim() == 2 and W.stride(1) == 1
+    N, K = W.shape
+    Wq = torch.empty((N, K // 2), dtype=torch.uint8, device=W.device)
+    Sw = torch.empty((K // group, N), dtype=torch.float32, device=W.device)
+    st = lib().comet_pack_weight(_ptr(W), W.stride(0), N, K, _ptr(perm), group, _ptr(Wq), _ptr(Sw), _stream(stream))
+    _check("comet_pack_weight", st)
+    return Wq, Sw
+
+
+def alloc_act_planes(M: int, K: int, bits, device):
+    b = as_bits(bits)
+    ldsx = comet_act_ldsx(M)
+    Xq8 = torch.empty((M, BLOCK * b.n8), dtype=torch.int8, device=device)
+    Xq4 = torch.empty((M, BLOCK * b.n4 // 2), dtype=torch.uint8, device=device)
+    Sx = torch.empty((K // BLOCK, ldsx), dtype=torch.float32, device=device)
+    return Xq8, Xq4, Sx
+
+
+def comet_quantize_act(X: torch.Tensor, bits, perm: Optional[torch.Tensor] = None, out=None, stream=None):
+    """a1+a2: X fp16 [M x K] -> (Xq8, Xq4, Sx)."""
+    assert X.is_cuda and X.dtype == torch.float16 and X.dim() == 2 and X.stride(1) == 1
+    b = as_bits(bits)
+    M, K = X.shape
+    Xq8, Xq4, Sx = out if out is not None else alloc_act_planes(M, K, b, X.device)
+    st = lib().comet_quantize_act(_ptr(X), X.stride(0), M, K, _ptr(perm), b.ptr, _ptr(Xq8) if b.n8 else None,
+                                  _ptr(Xq4) if b.n4 else None, _ptr(Sx), Sx.shape[1], _stream(stream))
+    _check("comet_quantize_act", st)
+    return Xq8, Xq4, Sx
+
+
+def comet_w4ax_gemm(Xq8, Xq4, Sx, bits, Wq, Sw, group: int = BLOCK, out: Optional[torch.Tensor] = None,
+                    workspace: Optional[torch.Tensor] = None, stream=None):
+    """a3..a8: Y fp16 [M x N] = dequant(Xq . Wq^T)."""
+    b = as_bits(bits)
+    M = Xq8.shape[0] if b.n8 else Xq4.shape[0]
+    N, K = Wq.shape[0], Wq.shape[1] * 2
+    Y = out if out is not None else torch.empty((M, N), dtype=torch.float16, device=Wq.device)
+    need = comet_w4ax_gemm_workspace_bytes(M, N, K)
+    if need > 0 and (workspace is None or workspace.numel() < need):
+        raise CometError("comet_w4ax_gemm", 4)
+    st = lib().comet_w4ax_gemm(_ptr(Xq8) if b.n8 else None, _ptr(Xq4) if b.n4 else None, _ptr(Sx), Sx.shape[1], b.ptr,
+                               M, K, _ptr(Wq), _ptr(Sw), N, group, _ptr(Y), Y.stride(0),
+                               _ptr(workspace), 0 if workspace is None else workspace.numel(), _stream(stream))
+    _check("comet_w4ax_gemm", st)
+    return Y
+
+
+def comet_w4ax_gemm_acc_i32(Xq8, Xq4, Sx, bits, Wq, Sw, group: int = BLOCK, stream=None):
+    """Debug: per-block INT32 accumulators [K/128 x M x N] (logical units)."""
+    b = as_bits(bits)
+    M = Xq8.shape[0] if b.n8 else Xq4.shape[0]
+    N, K = Wq.shape[0], Wq.shape[1] * 2
+    Acc = torch.empty((K // BLOCK, M, N), dtype=torch.int32, device=Wq.device)
+    st = lib().comet_w4ax_gemm_acc_i32(_ptr(Xq8) if b.n8 else None, _ptr(Xq4) if b.n4 else None, _ptr(Sx), Sx.shape[1],
+                                       b.ptr, M, K, _ptr(Wq), _ptr(Sw), N, group, _ptr(Acc), _stream(stream))
+    _check("comet_w4ax_gemm_acc_i32", st)
+    return Acc
+
+
+def comet_w4ax_linear(X: torch.Tensor, bits, Wq, Sw, perm=None, group: int = BLOCK, out: Optional[torch.Tensor] = None,
+                      scratch: Optional[torch.Tensor] = None, stream=None):
+    """Whole linear layer through the C ABI; X / out may be host (pinned) tensors."""
+    b = as_bits(bits)
+    M, K = X.shape
+    N = Wq.shape[0]
+    Y = out if out is not None else torch.empty((M, N), dtype=torch.float16, device=Wq.device)
+    need = comet_w4ax_linear_scratch_bytes(M, N, K, b)
+    if scratch is None or scratch.numel() < need:
+        raise CometError("comet_w4ax_linear", 4)
+    st = lib().comet_w4ax_linear(_ptr(X), X.stride(0), M, K, _ptr(perm), b.ptr, _ptr(Wq), _ptr(Sw), N, group,
+                                 _ptr(Y), Y.stride(0), _ptr(scratch), scratch.numel(), _stream(stream))
+    _check("comet_w4ax_linear", st)
+    return Y
+
+
+class W4AxLinear:
+    """A packed W4Ax linear layer: weights packed once (a0), forward = a1..a8."""
+
+    def __init__(self, W: torch.Tensor, bits, perm: Optional[torch.Tensor] = None, group: int = BLOCK):
+        self.bits = as_bits(bits)
+        self.perm = perm
+        self.group = group
+        self.N, self.K = W.shape
+        self.Wq, self.Sw = comet_pack_weight(W, perm, group)
+        self._ws = {}
+
+    def workspace(self, M: int):
+        need = comet_w4ax_gemm_workspace_bytes(M, self.N, self.K)
+        ws = self._ws.get(need)
+        if ws is None and need > 0:
+            ws = self._ws[need] = new_workspace(need, self.Wq.device)
+        return ws
+
+    def __call__(self, X: torch.Tensor, out: Optional[torch.Tensor] = None, planes=None):
+        Xq8, Xq4, Sx = comet_quantize_act(X, self.bits, self.perm, out=planes)
+        return comet_w4ax_gemm(Xq8, Xq4, Sx, self.bits, self.Wq, self.Sw, self.group, out=out,
+                               workspace=self.workspace(X.shape[0]))

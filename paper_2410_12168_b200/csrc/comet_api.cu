@@ -1,0 +1,417 @@
+// comet_api.cu -- host side of libcomet.so: argument validation, TMA tensor
+// map construction, launch heuristics and the extern "C" entry points
+// declared in include/comet.h.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+
+#include "../../include/comet.h"
+#include "gemm.cuh"
+#include "quantize.cuh"
+
+using namespace comet;
+
+namespace {
+
+thread_local char g_cuda_err[256] = "";
+std::atomic<int64_t> g_launches{0};
+
+comet_status cuda_fail(cudaError_t e) {
+  snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+  return COMET_ERR_CUDA;
+}
+comet_status check_launch() {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? COMET_OK : cuda_fail(e);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ---- device capability (cached once per device, thread-safe) -------------
+std::mutex g_dev_mu;
+int g_dev_ok[64];  // 0 unknown, 1 ok, -1 unsupported
+int g_num_sms[64];
+
+comet_status device_check(int* num_sms) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (dev < 0 || dev >= 64) return COMET_ERR_UNSUPPORTED;
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (g_dev_ok[dev] == 0) {
+    cudaDeviceProp prop;
+    e = cudaGetDeviceProperties(&prop, dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_dev_ok[dev] = (prop.major == 10 && prop.minor == 0) ? 1 : -1;
+    g_num_sms[dev] = prop.multiProcessorCount;
+  }
+  if (num_sms) *num_sms = g_num_sms[dev];
+  return g_dev_ok[dev] == 1 ? COMET_OK : COMET_ERR_UNSUPPORTED;
+}
+
+// ---- TMA tensor maps via the driver entry point (no -lcuda needed) ------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2-D uint8 tensor [rows x cols] (row stride ld bytes), box [box_rows x box_cols]
+bool make_map_u8(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t ld, uint32_t box_cols,
+                 uint32_t box_rows, CUtensorMapSwizzle swz) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// ---- block map ------------------------------------------------------------
+bool build_block_map(const uint8_t* bits, int nb, BlockMap* map, int* n8, int* n4) {
+  int r8 = 0, r4 = 0;
+  for (int b = 0; b < nb; ++b) {
+    if (bits[b] == 8) {
+      map->code[b] = (uint16_t)(0x8000u | r8++);
+    } else if (bits[b] == 4) {
+      map->code[b] = (uint16_t)(r4++);
+    } else {
+      return false;
+    }
+  }
+  for (int b = nb; b < 512; ++b) map->code[b] = 0;
+  if (n8) *n8 = r8;
+  if (n4) *n4 = r4;
+  return true;
+}
+
+// ---- GEMM launch plan -----------------------------------------------------
+struct Plan {
+  int bn, m_tiles, n_tiles, splits;
+  int64_t ws_bytes;
+};
+constexpr int64_t kCounterBytes = 64 * 1024;
+
+Plan make_plan(int M, int N, int K, int num_sms) {
+  Plan p;
+  p.bn = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128;
+  p.m_tiles = (M + p.bn - 1) / p.bn;
+  p.n_tiles = N / 128;
+  const int nb = K / 128;
+  const int tiles = p.m_tiles * p.n_tiles;
+  const int ctas_per_sm = p.bn <= 64 ? 2 : 1;
+  const int target = num_sms * ctas_per_sm;
+  p.splits = 1;
+  if (tiles > 0 && tiles < target) {
+    int s = (target + tiles / 2) / tiles;
+    int max_s = nb / 2 > 1 ? nb / 2 : 1;  // keep >= 2 blocks per split
+    p.splits = s < 1 ? 1 : (s > max_s ? max_s : s);
+    if (tiles > kCounterBytes / 4) p.splits = 1;
+  }
+  p.ws_bytes = p.splits > 1 ? kCounterBytes + (int64_t)tiles * p.splits * p.bn * 128 * 4 : 0;
+  return p;
+}
+
+int g_smem_attr_set[4][2];
+
+template <int BN, bool kAcc>
+comet_status launch_gemm_bn(const CUtensorMap& tmW, const CUtensorMap& tmX4, const CUtensorMap& tmX8,
+                            const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
+  using C = GemmCfg<BN>;
+  auto kern = w4ax_gemm_kernel<BN, kAcc>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes); });
+  if (attr_err != cudaSuccess) return cuda_fail(attr_err);
+  dim3 grid(p.n_tiles, p.m_tiles, p.splits);
+  kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(tmW, tmX4, tmX8, map, args);
+  return check_launch();
+}
+
+template <bool kAcc>
+comet_status launch_gemm(const CUtensorMap& tmW, const CUtensorMap& tmX4, const CUtensorMap& tmX8,
+                         const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
+  switch (p.bn) {
+    case 16: return launch_gemm_bn<16, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
+    case 32: return launch_gemm_bn<32, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
+    case 64: return launch_gemm_bn<64, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
+    default: return launch_gemm_bn<128, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
+  }
+}
+
+comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx, const uint8_t* bits,
+                         int32_t M, int32_t K, const void* Wq, const float* Sw, int32_t N, int32_t group, void* Y,
+                         int64_t ldy, int32_t* Acc, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (!bits || M < 0 || N < 0 || K <= 0) return COMET_ERR_INVALID_ARG;
+  if (K % 128 || N % 128 || K > 65536) return COMET_ERR_SHAPE;
+  if (group != 128 && group != K) return COMET_ERR_SHAPE;
+  if (ldsx < M || ldsx % 4) return COMET_ERR_SHAPE;
+  const int nb = K / 128;
+  BlockMap map;
+  int n8 = 0, n4 = 0;
+  if (!build_block_map(bits, nb, &map, &n8, &n4)) return COMET_ERR_INVALID_ARG;
+  if (M == 0 || N == 0) return COMET_OK;
+  if (!Wq || !Sx || (!Acc && (!Sw || !Y))) return COMET_ERR_INVALID_ARG;
+  if (Acc == nullptr && (ldy < N)) return COMET_ERR_SHAPE;
+  if ((n8 && !Xq8) || (n4 && !Xq4)) return COMET_ERR_INVALID_ARG;
+  if ((n8 && !aligned16(Xq8)) || (n4 && !aligned16(Xq4)) || !aligned16(Wq) || !aligned16(Sx))
+    return COMET_ERR_ALIGNMENT;
+  int num_sms = 148;
+  comet_status ds = device_check(&num_sms);
+  if (ds != COMET_OK) return ds;
+  Plan p = make_plan(M, N, K, num_sms);
+  if (!Acc && p.ws_bytes > 0 && (ws == nullptr || (int64_t)ws_bytes < p.ws_bytes)) return COMET_ERR_WORKSPACE;
+
+  CUtensorMap tmW, tmX4, tmX8;
+  if (!make_map_u8(&tmW, Wq, (uint64_t)K / 2, (uint64_t)N, (uint64_t)K / 2, 64, 128, CU_TENSOR_MAP_SWIZZLE_NONE))
+    return COMET_ERR_CUDA;
+  if (n4) {
+    if (!make_map_u8(&tmX4, Xq4, (uint64_t)n4 * 64, (uint64_t)M, (uint64_t)n4 * 64, 64, p.bn,
+                     CU_TENSOR_MAP_SWIZZLE_NONE))
+      return COMET_ERR_CUDA;
+  } else {
+    tmX4 = tmW;  // never dereferenced
+  }
+  if (n8) {
+    if (!make_map_u8(&tmX8, Xq8, (uint64_t)n8 * 128, (uint64_t)M, (uint64_t)n8 * 128, 128, p.bn,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+      return COMET_ERR_CUDA;
+  } else {
+    tmX8 = tmW;
+  }
+  GemmArgs a;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.nb = nb;
+  a.ldsx = ldsx;
+  a.ldy = ldy;
+  a.Sx = Sx;
+  a.Sw = Sw;
+  a.group_blocks = group / 128;
+  a.Y = reinterpret_cast<__half*>(Y);
+  a.Acc = Acc;
+  a.splits = p.splits;
+  a.ws_counter = reinterpret_cast<int*>(ws);
+  a.ws_partial = ws ? reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + kCounterBytes) : nullptr;
+  if (Acc) return launch_gemm<true>(tmW, tmX4, tmX8, map, a, p, st);
+  return launch_gemm<false>(tmW, tmX4, tmX8, map, a, p, st);
+}
+
+int64_t plane_bytes(int32_t M, int32_t K, const uint8_t* bits, int want) {
+  if (M < 0 || K <= 0 || K % 128 || !bits) return -1;
+  int64_t cnt = 0;
+  for (int b = 0; b < K / 128; ++b) {
+    if (bits[b] != 4 && bits[b] != 8) return -1;
+    if (bits[b] == want) ++cnt;
+  }
+  return want == 8 ? (int64_t)M * cnt * 128 : (int64_t)M * cnt * 64;
+}
+
+int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
+
+}  // namespace
+
+extern "C" {
+
+int64_t comet_act_plane8_bytes(int32_t M, int32_t K, const uint8_t* block_bits) { return plane_bytes(M, K, block_bits, 8); }
+int64_t comet_act_plane4_bytes(int32_t M, int32_t K, const uint8_t* block_bits) { return plane_bytes(M, K, block_bits, 4); }
+int64_t comet_act_ldsx(int32_t M) { return M < 0 ? -1 : ((int64_t)M + 3) / 4 * 4; }
+
+int64_t comet_w4ax_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K) {
+  if (M < 0 || N < 0 || K <= 0 || K % 128 || N % 128) return -1;
+  if (M == 0 || N == 0) return 0;
+  int num_sms = 148;
+  if (device_check(&num_sms) != COMET_OK) num_sms = 148;
+  return make_plan(M, N, K, num_sms).ws_bytes;
+}
+
+int64_t comet_w4ax_linear_scratch_bytes(int32_t M, int32_t N, int32_t K, const uint8_t* block_bits) {
+  int64_t p8 = plane_bytes(M, K, block_bits, 8), p4 = plane_bytes(M, K, block_bits, 4);
+  int64_t ws = comet_w4ax_gemm_workspace_bytes(M, N, K);
+  if (p8 < 0 || p4 < 0 || ws < 0) return -1;
+  int64_t sx = (K / 128) * comet_act_ldsx(M) * 4;
+  int64_t io = align256((int64_t)M * K * 2) + align256((int64_t)M * N * 2);  // staging for host X / Y
+  return align256(ws > 0 ? ws : 0) + align256(p8) + align256(p4) + align256(sx) + align256(io) + 256;
+}
+
+comet_status comet_pack_weight(const void* W, int64_t ldw, int32_t N, int32_t K, const int32_t* perm, int32_t group,
+                               void* Wq, float* Sw, comet_stream_t stream) {
+  if (N < 0 || K <= 0) return COMET_ERR_INVALID_ARG;
+  if (K % 128 || K > 65536 || (group != 128 && group != K) || ldw < K || ldw % 8) return COMET_ERR_SHAPE;
+  if (N == 0) return COMET_OK;
+  if (!W || !Wq || !Sw) return COMET_ERR_INVALID_ARG;
+  if (!aligned16(W) || !aligned16(Wq) || (perm && !aligned16(perm))) return COMET_ERR_ALIGNMENT;
+  comet_status ds = device_check(nullptr);
+  if (ds != COMET_OK) return ds;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const __half* Wh = reinterpret_cast<const __half*>(W);
+  if (group == 128) {
+    // group-128 weights are "activations" with an all-INT4 mask, Sw = Sx with ldsx = N
+    BlockMap map;
+    for (int b = 0; b < 512; ++b) map.code[b] = (uint16_t)(b < K / 128 ? b : 0);
+    const int64_t items = ((int64_t)N + 7) / 8 * 8 * (K / 128);
+    int grid = (int)((items + 15) / 16);
+    if (grid > 148 * 16) grid = 148 * 16;
+    // Sw layout [K/128 x N] is the Sx layout with ldsx == N (no padding rows)
+    if (perm)
+      quantize_act_kernel<true><<<grid, 256, 0, st>>>(Wh, ldw, N, K / 128, N, perm, map, nullptr, 0,
+                                                       reinterpret_cast<uint8_t*>(Wq), K / 2, Sw);
+    else
+      quantize_act_kernel<false><<<grid, 256, 0, st>>>(Wh, ldw, N, K / 128, N, perm, map, nullptr, 0,
+                                                        reinterpret_cast<uint8_t*>(Wq), K / 2, Sw);
+  } else {
+    int grid = (N + 7) / 8;
+    if (perm)
+      pack_weight_rowscale_kernel<true><<<grid, 256, 0, st>>>(Wh, ldw, N, K, perm, reinterpret_cast<uint8_t*>(Wq), Sw);
+    else
+      pack_weight_rowscale_kernel<false><<<grid, 256, 0, st>>>(Wh, ldw, N, K, perm, reinterpret_cast<uint8_t*>(Wq), Sw);
+  }
+  return check_launch();
+}
+
+comet_status comet_quantize_act(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
+                                const uint8_t* block_bits, int8_t* Xq8, void* Xq4, float* Sx, int64_t ldsx,
+                                comet_stream_t stream) {
+  if (M < 0 || K <= 0 || !block_bits) return COMET_ERR_INVALID_ARG;
+  if (K % 128 || K > 65536 || ldx < K || ldx % 8 || ldsx < M || ldsx % 4) return COMET_ERR_SHAPE;
+  BlockMap map;
+  int n8 = 0, n4 = 0;
+  if (!build_block_map(block_bits, K / 128, &map, &n8, &n4)) return COMET_ERR_INVALID_ARG;
+  if (M == 0) return COMET_OK;
+  if (!X || !Sx || (n8 && !Xq8) || (n4 && !Xq4)) return COMET_ERR_INVALID_ARG;
+  if (!aligned16(X) || (n8 && !aligned16(Xq8)) || (n4 && !aligned16(Xq4)) || !aligned16(Sx) ||
+      (perm && !aligned16(perm)))
+    return COMET_ERR_ALIGNMENT;
+  int num_sms = 148;
+  comet_status ds = device_check(&num_sms);
+  if (ds != COMET_OK) return ds;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t items = (ldsx + 7) / 8 * 8 * (K / 128);
+  int64_t grid = (items + 15) / 16;
+  if (grid > (int64_t)num_sms * 16) grid = (int64_t)num_sms * 16;
+  const __half* Xh = reinterpret_cast<const __half*>(X);
+  if (perm)
+    quantize_act_kernel<true><<<(int)grid, 256, 0, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
+                                                          reinterpret_cast<uint8_t*>(Xq4), (int64_t)n4 * 64, Sx);
+  else
+    quantize_act_kernel<false><<<(int)grid, 256, 0, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
+                                                           reinterpret_cast<uint8_t*>(Xq4), (int64_t)n4 * 64, Sx);
+  return check_launch();
+}
+
+comet_status comet_w4ax_gemm(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
+                             const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq, const float* Sw,
+                             int32_t N, int32_t group, void* Y, int64_t ldy, void* workspace, size_t workspace_bytes,
+                             comet_stream_t stream) {
+  return gemm_common(Xq8, Xq4, Sx, ldsx, block_bits, M, K, Wq, Sw, N, group, Y, ldy, nullptr, workspace,
+                     workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+comet_status comet_w4ax_gemm_acc_i32(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
+                                     const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq,
+                                     const float* Sw, int32_t N, int32_t group, int32_t* Acc, comet_stream_t stream) {
+  if (M > 0 && N > 0 && !Acc) return COMET_ERR_INVALID_ARG;
+  return gemm_common(Xq8, Xq4, Sx, ldsx, block_bits, M, K, Wq, Sw, N, group, nullptr, N, Acc, nullptr, 0,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
+                               const uint8_t* block_bits, const void* Wq, const float* Sw, int32_t N, int32_t group,
+                               void* Y, int64_t ldy, void* scratch, size_t scratch_bytes, comet_stream_t stream) {
+  if (M < 0 || N < 0 || K <= 0 || !block_bits) return COMET_ERR_INVALID_ARG;
+  if (K % 128 || N % 128 || ldx < K || ldy < N || ldx % 8 || ldy % 8) return COMET_ERR_SHAPE;
+  const int64_t need = comet_w4ax_linear_scratch_bytes(M, N, K, block_bits);
+  if (need < 0) return COMET_ERR_INVALID_ARG;
+  if (M == 0 || N == 0) return COMET_OK;
+  if (!X || !Y || !Wq || !Sw) return COMET_ERR_INVALID_ARG;
+  if (!scratch || (int64_t)scratch_bytes < need) return COMET_ERR_WORKSPACE;
+  comet_status ds = device_check(nullptr);
+  if (ds != COMET_OK) return ds;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaPointerAttributes ax, ay;
+  cudaError_t e = cudaPointerGetAttributes(&ax, X);
+  if (e != cudaSuccess) return cuda_fail(e);
+  e = cudaPointerGetAttributes(&ay, Y);
+  if (e != cudaSuccess) return cuda_fail(e);
+  const bool x_host = ax.type != cudaMemoryTypeDevice && ax.type != cudaMemoryTypeManaged;
+  const bool y_host = ay.type != cudaMemoryTypeDevice && ay.type != cudaMemoryTypeManaged;
+
+  char* p = reinterpret_cast<char*>(scratch);
+  const int64_t ws_bytes = comet_w4ax_gemm_workspace_bytes(M, N, K);
+  void* ws = ws_bytes > 0 ? p : nullptr;  // counters must stay at the scratch base (zeroed once)
+  p += align256(ws_bytes > 0 ? ws_bytes : 0);
+  const int64_t p8 = plane_bytes(M, K, block_bits, 8), p4 = plane_bytes(M, K, block_bits, 4);
+  int8_t* Xq8 = reinterpret_cast<int8_t*>(p);
+  p += align256(p8);
+  void* Xq4 = p;
+  p += align256(p4);
+  const int64_t ldsx = comet_act_ldsx(M);
+  float* Sx = reinterpret_cast<float*>(p);
+  p += align256((K / 128) * ldsx * 4);
+  const void* Xd = X;
+  int64_t ldxd = ldx;
+  if (x_host) {  // stage the host rows densely (ld = K) in scratch
+    void* xs = p;
+    p += align256((int64_t)M * K * 2);
+    e = cudaMemcpy2DAsync(xs, (size_t)K * 2, X, (size_t)ldx * 2, (size_t)K * 2, (size_t)M, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e);
+    Xd = xs;
+    ldxd = K;
+  }
+  void* Yd = Y;
+  int64_t ldyd = ldy;
+  if (y_host) {
+    Yd = p;
+    ldyd = N;
+  }
+  comet_status s = comet_quantize_act(Xd, ldxd, M, K, perm, block_bits, Xq8, Xq4, Sx, ldsx, stream);
+  if (s != COMET_OK) return s;
+  s = comet_w4ax_gemm(Xq8, Xq4, Sx, ldsx, block_bits, M, K, Wq, Sw, N, group, Yd, ldyd, ws,
+                      ws_bytes > 0 ? (size_t)ws_bytes : 0, stream);
+  if (s != COMET_OK) return s;
+  if (y_host) {
+    e = cudaMemcpy2DAsync(Y, (size_t)ldy * 2, Yd, (size_t)N * 2, (size_t)N * 2, (size_t)M, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(e);
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  return COMET_OK;
+}
+
+const char* comet_status_str(comet_status s) {
+  switch (s) {
+    case COMET_OK: return "COMET_OK";
+    case COMET_ERR_INVALID_ARG: return "COMET_ERR_INVALID_ARG";
+    case COMET_ERR_SHAPE: return "COMET_ERR_SHAPE";
+    case COMET_ERR_ALIGNMENT: return "COMET_ERR_ALIGNMENT";
+    case COMET_ERR_WORKSPACE: return "COMET_ERR_WORKSPACE";
+    case COMET_ERR_UNSUPPORTED: return "COMET_ERR_UNSUPPORTED";
+    case COMET_ERR_CUDA: return "COMET_ERR_CUDA";
+  }
+  return "COMET_ERR_UNKNOWN";
+}
+
+const char* comet_last_cuda_error(void) { return g_cuda_err; }
+int64_t comet_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

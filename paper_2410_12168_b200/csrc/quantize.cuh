@@ -1,0 +1,158 @@
+// quantize.cuh -- a1+a2 (FMPQ activation quantize/pack, P:L185 + P:L194 §3.2)
+// and a0 (INT4 weight pack, P:L194 + P:L396) for sm_100a.
+//
+// Work unit: one (row, 128-channel block) "item" is handled by a half-warp;
+// each lane owns 8 consecutive (permuted) channels = one 128-bit fp16 load,
+// one 32-bit INT4 store (or one 64-bit INT8 store).  The block absmax is a
+// 4-step shuffle reduction inside the half-warp.  Items are ordered
+// block-major inside groups of 8 rows so the Sx writes of a warp-pair are
+// contiguous.  HBM-bound: algorithmic bytes per element ~ 2 (fp16 in)
+// + 0.5..1 (plane out) + 4/128 (scale).
+#pragma once
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "sm100.cuh"
+
+namespace comet {
+
+struct BlockMap {
+  // per 128-channel block: bit 15 = INT8 block, bits 0..14 = rank in its plane
+  uint16_t code[512];
+};
+
+DEVI float half_bits_to_float(uint32_t h) { return __half2float(__ushort_as_half((unsigned short)h)); }
+
+// round half away from zero of v, exact for |v| < 2^23:
+// floor(RZ(|v| + 0.5)) == floor(|v| + 0.5) because RZ never crosses the
+// integer just below the exact sum.
+DEVI int32_t round_half_away(float v) {
+  int32_t q = __float2int_rz(__fadd_rz(fabsf(v), 0.5f));
+  return v < 0.0f ? -q : q;
+}
+
+// Quantize 8 values with reciprocal r (already IEEE qmax/a) into int8.
+DEVI void quant8(const float (&x)[8], float r, int32_t (&q)[8]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) q[j] = round_half_away(__fmul_rn(x[j], r));
+}
+
+DEVI uint32_t pack_int4_word(const int32_t (&q)[8]) {
+  uint32_t w = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) w |= ((uint32_t)(q[j] & 0xF) | ((uint32_t)(q[j + 4] & 0xF) << 4)) << (8 * j);
+  return w;
+}
+
+// Load the lane's 8 channels of row m, block b (positions 128b + 8*o .. +7
+// on the permuted axis).
+template <bool kPerm>
+DEVI void load_octet(const __half* __restrict__ X, int64_t ldx, int64_t m, int b, int o, const int32_t* __restrict__ perm,
+                     float (&x)[8]) {
+  const int i0 = b * 128 + o * 8;
+  if (!kPerm) {
+    uint4 v = __ldg(reinterpret_cast<const uint4*>(X + m * ldx + i0));
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      x[2 * j] = half_bits_to_float(w[j] & 0xFFFF);
+      x[2 * j + 1] = half_bits_to_float(w[j] >> 16);
+    }
+  } else {
+    int4 p0 = __ldg(reinterpret_cast<const int4*>(perm + i0));
+    int4 p1 = __ldg(reinterpret_cast<const int4*>(perm + i0 + 4));
+    int p[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+    const unsigned short* row = reinterpret_cast<const unsigned short*>(X + m * ldx);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = half_bits_to_float(__ldg(row + p[j]));
+  }
+}
+
+// Activation quantize + pack.  rows = ldsx (rows >= M get only Sx = 1.0).
+template <bool kPerm>
+__global__ void __launch_bounds__(256) quantize_act_kernel(const __half* __restrict__ X, int64_t ldx, int M, int nb,
+                                                           int64_t ldsx, const int32_t* __restrict__ perm,
+                                                           const __grid_constant__ BlockMap map, int8_t* __restrict__ Xq8,
+                                                           int64_t ld8, uint8_t* __restrict__ Xq4, int64_t ld4,
+                                                           float* __restrict__ Sx) {
+  const int half_id = threadIdx.x >> 4;  // 16 half-warps per CTA
+  const int o = threadIdx.x & 15;        // octet within the block
+  const unsigned hmask = 0xFFFFu << (threadIdx.x & 16);  // this half-warp's lanes
+  const int64_t n_groups = (ldsx + 7) / 8;
+  const int64_t items = n_groups * 8 * nb;
+  for (int64_t it = (int64_t)blockIdx.x * 16 + half_id; it < items; it += (int64_t)gridDim.x * 16) {
+    const int64_t g = it / (8 * nb);
+    const int rem = (int)(it - g * 8 * nb);
+    const int b = rem >> 3;
+    const int64_t m = g * 8 + (rem & 7);
+    if (m >= ldsx) continue;
+    if (m >= M) {
+      if (o == 0) Sx[(int64_t)b * ldsx + m] = 1.0f;
+      continue;
+    }
+    float x[8];
+    load_octet<kPerm>(X, ldx, m, b, o, perm, x);
+    float a = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a = fmaxf(a, fabsf(x[j]));
+#pragma unroll
+    for (int off = 8; off >= 1; off >>= 1) a = fmaxf(a, __shfl_xor_sync(hmask, a, off));
+    const uint32_t code = map.code[b];
+    const bool is8 = (code >> 15) != 0;
+    const int rank = code & 0x7FFF;
+    const float qmax = is8 ? 127.0f : 7.0f;
+    float s = 1.0f, r = 0.0f;
+    if (a != 0.0f) {
+      s = __fdiv_rn(a, qmax);
+      r = __fdiv_rn(qmax, a);
+    }
+    int32_t q[8];
+    quant8(x, r, q);
+    if (is8) {
+      uint32_t lo = (uint32_t)(q[0] & 0xFF) | ((uint32_t)(q[1] & 0xFF) << 8) | ((uint32_t)(q[2] & 0xFF) << 16) |
+                    ((uint32_t)(q[3] & 0xFF) << 24);
+      uint32_t hi = (uint32_t)(q[4] & 0xFF) | ((uint32_t)(q[5] & 0xFF) << 8) | ((uint32_t)(q[6] & 0xFF) << 16) |
+                    ((uint32_t)(q[7] & 0xFF) << 24);
+      *reinterpret_cast<uint2*>(Xq8 + m * ld8 + (int64_t)rank * 128 + o * 8) = make_uint2(lo, hi);
+    } else {
+      *reinterpret_cast<uint32_t*>(Xq4 + m * ld4 + (int64_t)rank * 64 + o * 4) = pack_int4_word(q);
+    }
+    if (o == 0) Sx[(int64_t)b * ldsx + m] = s;
+  }
+}
+
+// Weight pack with one scale per output channel (group == K): a warp per
+// row, pass 1 = absmax over the permuted row, pass 2 = quantize + pack.
+template <bool kPerm>
+__global__ void __launch_bounds__(256) pack_weight_rowscale_kernel(const __half* __restrict__ W, int64_t ldw, int N,
+                                                                   int K, const int32_t* __restrict__ perm,
+                                                                   uint8_t* __restrict__ Wq, float* __restrict__ Sw) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n = (int64_t)blockIdx.x * 8 + warp;
+  if (n >= N) return;
+  const int n_oct = K / 8;
+  float a = 0.0f;
+  for (int t = lane; t < n_oct; t += 32) {
+    float x[8];
+    load_octet<kPerm>(W, ldw, n, t >> 4, t & 15, perm, x);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a = fmaxf(a, fabsf(x[j]));
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, off));
+  float s = 1.0f, r = 0.0f;
+  if (a != 0.0f) {
+    s = __fdiv_rn(a, 7.0f);
+    r = __fdiv_rn(7.0f, a);
+  }
+  for (int t = lane; t < n_oct; t += 32) {
+    float x[8];
+    load_octet<kPerm>(W, ldw, n, t >> 4, t & 15, perm, x);
+    int32_t q[8];
+    quant8(x, r, q);
+    *reinterpret_cast<uint32_t*>(Wq + n * (K / 2) + (int64_t)t * 4) = pack_int4_word(q);
+  }
+  if (lane == 0) Sw[n] = s;
+}
+
+}  // namespace comet

@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle (-m gpu).
+
+Bars (BJ north_star):
+  * packed planes Xq8/Xq4, scales Sx, packed weights Wq and Sw: bit-exact;
+  * per-block INT32 accumulators (comet_w4ax_gemm_acc_i32): bit-exact;
+  * Y fp16: |y - y_ref| <= max(2^-10 |y_ref|, 1e-3) elementwise.
+Inputs come from paper_2410_12168_b200.synth (seeded); expected values only
+from oracle/.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2410_12168_b200 import comet, synth
+
+pytestmark = pytest.mark.gpu
+
+REL, ABS = 2.0 ** -10, 1e-3
+
+
+def to_dev(a):
+    return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def gpu_path(p, group, want_acc=False, planes_only=False):
+    X, W = to_dev(p["X"]), to_dev(p["W"])
+    perm = to_dev(p["perm"])
+    bits = comet.BlockBits(p["bits"])
+    Wq, Sw = comet.comet_pack_weight(W, perm, group)
+    Xq8, Xq4, Sx = comet.comet_quantize_act(X, bits, perm)
+    out = {"Wq": Wq, "Sw": Sw, "Xq8": Xq8, "Xq4": Xq4, "Sx": Sx}
+    if not planes_only:
+        M, N, K = X.shape[0], W.shape[0], X.shape[1]
+        ws = comet.new_workspace(comet.comet_w4ax_gemm_workspace_bytes(M, N, K), X.device)
+        out["Y"] = comet.comet_w4ax_gemm(Xq8, Xq4, Sx, bits, Wq, Sw, group, workspace=ws)
+        if want_acc:
+            out["Acc"] = comet.comet_w4ax_gemm_acc_i32(Xq8, Xq4, Sx, bits, Wq, Sw, group)
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in out.items()}
+
+
+def oracle_path(p, group, rows=None, want_acc=False):
+    Xq8, Xq4, Sx = oracle.quantize_act(p["X"], p["bits"], p["perm"])
+    Wq, Sw = oracle.pack_weight(p["W"], group, p["perm"])
+    r = oracle.w4ax_gemm(Xq8, Xq4, Sx, p["bits"], Wq, Sw, group=group, rows=rows, want_acc=want_acc, want_y64=True)
+    return {"Xq8": Xq8, "Xq4": Xq4, "Sx": Sx, "Wq": Wq, "Sw": Sw, **r}
+
+
+def assert_planes_equal(g, o):
+    for k in ("Xq8", "Xq4", "Wq"):
+        assert g[k].shape == o[k].shape, k
+        assert np.array_equal(g[k].view(np.uint8), o[k].view(np.uint8)), k
+    for k in ("Sx", "Sw"):
+        assert np.array_equal(g[k].view(np.uint32), o[k].view(np.uint32)), k
+
+
+def assert_y_close(y_gpu, y_ref16, y64):
+    ref = y_ref16.astype(np.float64)
+    yg = y_gpu.astype(np.float64)
+    tol = np.maximum(REL * np.abs(ref), ABS)
+    bad = np.abs(yg - ref) > tol
+    assert not bad.any(), f"{bad.sum()} mismatches, worst {np.abs(yg - ref)[bad].max()}"
+    assert np.all(np.abs(yg - y64) <= np.maximum(REL * np.abs(y64), ABS) + np.abs(ref - y64))
+
+
+# ------------------------------------------------------------- C1 tiny ----
+C1_MASKS = [[8, 4, 4, 4], [4, 4, 8, 4], [4, 4, 4, 4], [8, 8, 8, 8]]
+
+
+@pytest.mark.parametrize("mask", C1_MASKS)
+@pytest.mark.parametrize("group", [128, 512])
+@pytest.mark.parametrize("seed", [0, 1])
+def test_c1_tiny_full_parity(mask, group, seed):
+    """BJ configs[0]: M=16 N=256 K=512, block 128, one INT8 outlier block."""
+    n8 = sum(1 for b in mask if b == 8)
+    p = synth.make_problem(16, 256, 512, n8=n8, seed=seed, mask=mask)
+    g = gpu_path(p, group, want_acc=True)
+    o = oracle_path(p, group, want_acc=True)
+    assert_planes_equal(g, o)
+    assert np.array_equal(g["Acc"], o["acc"])
+    assert_y_close(g["Y"], o["y"], o["y64"])
+
+
+@pytest.mark.parametrize("M", [1, 3, 5, 13, 16, 17, 31, 33, 64, 65, 100, 128, 129, 255, 300])
+def test_ragged_m_all_tile_widths(M):
+    """Every BN specialisation (16/32/64/128) and ragged token tails."""
+    p = synth.make_problem(M, 384, 1024, n8=1, seed=100 + M, mask="scattered")
+    g = gpu_path(p, 128, want_acc=True)
+    o = oracle_path(p, 128, want_acc=True)
+    assert_planes_equal(g, o)
+    assert np.array_equal(g["Acc"], o["acc"])
+    assert_y_close(g["Y"], o["y"], o["y64"])
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 4096, 4096), (16, 1024, 4096), (8, 512, 8192), (200, 256, 2048)])
+def test_split_k_decode_shapes(M, N, K):
+    """Few tiles -> split-K with the deterministic last-CTA fixup (a7)."""
+    assert comet.comet_w4ax_gemm_workspace_bytes(M, N, K) > 0
+    p = synth.make_problem(M, N, K, n8=K // 128 // 10, seed=7)
+    g = gpu_path(p, 128)
+    o = oracle_path(p, 128)
+    assert_planes_equal(g, o)
+    assert_y_close(g["Y"], o["y"], o["y64"])
+
+
+def test_no_permutation_and_outliers_unclustered():
+    p = synth.make_problem(48, 256, 1024, n8=2, seed=3, with_perm=False)
+    g = gpu_path(p, 128, want_acc=True)
+    o = oracle_path(p, 128, want_acc=True)
+    assert_planes_equal(g, o)
+    assert np.array_equal(g["Acc"], o["acc"])
+    assert_y_close(g["Y"], o["y"], o["y64"])
+
+
+def test_permutation_equivalence_on_gpu():
+    """P8: fused gather == pre-permuted input, bit-identical planes and Y."""
+    p = synth.make_problem(64, 256, 1024, n8=1, seed=5)
+    q = dict(p)
+    q["X"] = np.ascontiguousarray(p["X"][:, p["perm"]])
+    q["W"] = np.ascontiguousarray(p["W"][:, p["perm"]])
+    q["perm"] = None
+    a, b = gpu_path(p, 128), gpu_path(q, 128)
+    for k in a:
+        assert np.array_equal(a[k].view(np.uint8), b[k].view(np.uint8)), k
+
+
+def test_power_of_two_scales_bit_exact():
+    """P11: exact scales and products -> GPU fp16 Y bit-equal to the oracle."""
+    rng = np.random.default_rng(12)
+    M, N, K = 32, 256, 512
+    X = rng.integers(-7, 8, (M, K)).astype(np.float64)
+    X[:, :128] = rng.integers(-127, 128, (M, 128)) * 0.25
+    X[:, 0], X[:, 128], X[:, 256], X[:, 384] = 127 * 0.25, 7, -7, 7
+    W = rng.integers(-7, 8, (N, K)).astype(np.float64) * 0.5
+    W[:, 0::128] = 3.5
+    p = {"X": X.astype(np.float16), "W": W.astype(np.float16), "perm": None, "bits": np.array([8, 4, 4, 4], np.uint8)}
+    g = gpu_path(p, 128)
+    o = oracle_path(p, 128)
+    assert np.array_equal(o["y64"], X @ W.T)
+    assert np.array_equal(g["Y"].view(np.uint16), o["y"].view(np.uint16))
+
+
+def test_zero_padded_brute_force_8x8x64():
+    """P9 on the GPU: real 8x8x64 problem zero-padded to the ABI shape
+    (M=8, N=128, K=128) equals the k=64 oracle in the 8x8 corner."""
+    rng = np.random.default_rng(10)
+    X = (rng.standard_normal((8, 64)) * 2).astype(np.float16)
+    W = (rng.standard_normal((8, 64)) / 8).astype(np.float16)
+    b64 = np.array([4], np.uint8)
+    r64 = oracle.w4ax_gemm(*oracle.quantize_act(X, b64, None, k=64), b64, *oracle.pack_weight(W, 64), group=64, k=64,
+                           want_y64=True)
+    Xp = np.zeros((8, 128), np.float16)
+    Xp[:, :64] = X
+    Wp = np.zeros((128, 128), np.float16)
+    Wp[:8, :64] = W
+    g = gpu_path({"X": Xp, "W": Wp, "perm": None, "bits": np.array([4], np.uint8)}, 128)
+    assert_y_close(g["Y"][:, :8], r64["y64"].astype(np.float16), r64["y64"])
+    assert not g["Y"][:, 8:].any()
+
+
+def test_zero_blocks_and_zero_rows():
+    """A-7: all-zero blocks get s = 1 and q = 0; zero weight rows give Y = 0."""
+    p = synth.make_problem(20, 256, 512, n8=1, seed=4)
+    p["X"][3, :] = 0
+    p["X"][5, 128:256] = 0
+    p["W"][7, :] = 0
+    g = gpu_path(p, 128, want_acc=True)
+    o = oracle_path(p, 128, want_acc=True)
+    assert_planes_equal(g, o)
+    assert np.array_equal(g["Acc"], o["acc"])
+    assert not g["Y"][3].any() and not g["Y"][:, 7].any()
+
+
+def test_determinism():
+    p = synth.make_problem(16, 2048, 4096, n8=3, seed=8)
+    a, b = gpu_path(p, 128), gpu_path(p, 128)
+    assert np.array_equal(a["Y"].view(np.uint16), b["Y"].view(np.uint16))
+
+
+def test_fp16_extremes_quantize_bit_exact():
+    """Adversarial activations: +-65504, subnormals, -0, exact ties."""
+    rng = np.random.default_rng(2)
+    X = rng.standard_normal((8, 512)).astype(np.float16)
+    X[0, :8] = [65504, -65504, 6e-8, -6e-8, -0.0, 0.5, 1.5, 2.5]
+    X[1, :128] = np.float16(6e-8) * rng.integers(-20, 20, 128)  # subnormal block
+    X[2, 128:136] = [7, 3.5, -3.5, 1.5, 0.5, -0.5, 2.5, -2.5]    # ties at r == 1
+    X[3, 256:384] = 0
+    p = {"X": X, "W": np.zeros((128, 512), np.float16), "perm": None, "bits": np.array([4, 4, 8, 4], np.uint8)}
+    g = gpu_path(p, 128, planes_only=True)
+    o = oracle_path(p, 128)
+    for k in ("Xq8", "Xq4", "Sx"):
+        assert np.array_equal(g[k].view(np.uint8), o[k].view(np.uint8)), k
+
+
+def test_quantize_random_rows_bit_exact_large():
+    """10^5-ish random rows across scales: planes and scales bit-exact."""
+    rng = np.random.default_rng(77)
+    M, K = 4096, 1024
+    X = (rng.standard_normal((M, K)) * 10.0 ** rng.uniform(-4, 4, (M, 1))).astype(np.float16)
+    bits = synth.block_bits_for(K, 2, "scattered")
+    p = {"X": X, "W": np.zeros((128, K), np.float16), "perm": None, "bits": bits}
+    g = gpu_path(p, 128, planes_only=True)
+    Xq8, Xq4, Sx = oracle.quantize_act(X, bits)
+    assert np.array_equal(g["Xq8"], Xq8) and np.array_equal(g["Xq4"], Xq4)
+    assert np.array_equal(g["Sx"].view(np.uint32), Sx.view(np.uint32))
+
+
+# ------------------------------------------------- full-size (sampled) ----
+@pytest.mark.parametrize("M,N,K,n8", [(4096, 11008, 4096, 3), (16, 57344, 8192, 6), (2048, 8192, 28672, 22)])
+def test_full_size_sampled_rows(M, N, K, n8):
+    """BJ configs at full size in the launch configuration bench.py times:
+    planes/scales bit-exact over ALL rows; INT32 + Y on a 64-row sample."""
+    p = synth.make_problem(M, N, K, n8=n8, seed=300)
+    g = gpu_path(p, 128)
+    Xq8, Xq4, Sx = oracle.quantize_act(p["X"], p["bits"], p["perm"])
+    assert np.array_equal(g["Xq8"], Xq8) and np.array_equal(g["Xq4"], Xq4)
+    assert np.array_equal(g["Sx"].view(np.uint32), Sx.view(np.uint32))
+    Wq, Sw = oracle.pack_weight(p["W"], 128, p["perm"])
+    assert np.array_equal(g["Wq"], Wq) and np.array_equal(g["Sw"].view(np.uint32), Sw.view(np.uint32))
+    rows = synth.sample_rows(M, 64 if M > 64 else M)
+    r = oracle.w4ax_gemm(Xq8, Xq4, Sx, p["bits"], Wq, Sw, rows=rows, want_y64=True)
+    assert_y_close(g["Y"][rows], r["y"], r["y64"])
+
+
+def test_linear_entry_with_host_buffers():
+    """comet_w4ax_linear: host X in, host Y out, same result as the device path."""
+    p = synth.make_problem(100, 512, 1024, n8=1, seed=9)
+    g = gpu_path(p, 128)
+    W = to_dev(p["W"])
+    perm = to_dev(p["perm"])
+    bits = comet.BlockBits(p["bits"])
+    Wq, Sw = comet.comet_pack_weight(W, perm, 128)
+    Xh = torch.from_numpy(p["X"]).pin_memory()
+    Yh = torch.empty((100, 512), dtype=torch.float16).pin_memory()
+    scratch = comet.new_workspace(comet.comet_w4ax_linear_scratch_bytes(100, 512, 1024, bits), W.device)
+    comet.comet_w4ax_linear(Xh, bits, Wq, Sw, perm=perm, out=Yh, scratch=scratch)
+    assert np.array_equal(Yh.numpy().view(np.uint16), g["Y"].view(np.uint16))
