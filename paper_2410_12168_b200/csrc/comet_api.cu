@@ -11,6 +11,7 @@
 
 #include "../../include/comet.h"
 #include "gemm.cuh"
+#include "gemm_2sm.cuh"
 #include "quantize.cuh"
 
 using namespace comet;
@@ -107,12 +108,22 @@ bool build_block_map(const uint8_t* bits, int nb, BlockMap* map, int* n8, int* n
 // ---- GEMM launch plan -----------------------------------------------------
 struct Plan {
   int bn, m_tiles, n_tiles, splits;
+  bool two_sm;  // prefill: CTA-pair kernel (256 tokens x 256 weight rows per pair)
   int64_t ws_bytes;
 };
 constexpr int64_t kCounterBytes = 64 * 1024;
 
 Plan make_plan(int M, int N, int K, int num_sms) {
   Plan p;
+  p.two_sm = M > 128;
+  if (p.two_sm) {
+    p.bn = 128;  // token rows per CTA (TMA box height)
+    p.m_tiles = (M + 255) / 256;
+    p.n_tiles = (N + 255) / 256;
+    p.splits = 1;
+    p.ws_bytes = 0;
+    return p;
+  }
   p.bn = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128;
   p.m_tiles = (M + p.bn - 1) / p.bn;
   p.n_tiles = N / 128;
@@ -131,8 +142,6 @@ Plan make_plan(int M, int N, int K, int num_sms) {
   return p;
 }
 
-int g_smem_attr_set[4][2];
-
 template <int BN, bool kAcc>
 comet_status launch_gemm_bn(const CUtensorMap& tmW, const CUtensorMap& tmX4, const CUtensorMap& tmX8,
                             const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
@@ -147,9 +156,27 @@ comet_status launch_gemm_bn(const CUtensorMap& tmW, const CUtensorMap& tmX4, con
   return check_launch();
 }
 
+template <bool kGroupK, bool kAcc>
+comet_status launch_gemm_2sm(const CUtensorMap& tmW, const CUtensorMap& tmX4, const CUtensorMap& tmX8,
+                             const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
+  using C = Gemm2Cfg;
+  auto kern = w4ax_gemm_2sm_kernel<kGroupK, kAcc>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes); });
+  if (attr_err != cudaSuccess) return cuda_fail(attr_err);
+  dim3 grid(2 * p.m_tiles, p.n_tiles, 1);
+  kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(tmW, tmX4, tmX8, map, args);
+  return check_launch();
+}
+
 template <bool kAcc>
 comet_status launch_gemm(const CUtensorMap& tmW, const CUtensorMap& tmX4, const CUtensorMap& tmX8,
                          const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
+  if (p.two_sm) {
+    if (args.group_blocks == args.nb) return launch_gemm_2sm<true, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
+    return launch_gemm_2sm<false, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
+  }
   switch (p.bn) {
     case 16: return launch_gemm_bn<16, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
     case 32: return launch_gemm_bn<32, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
@@ -171,7 +198,9 @@ comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, in
   if (!build_block_map(bits, nb, &map, &n8, &n4)) return COMET_ERR_INVALID_ARG;
   if (M == 0 || N == 0) return COMET_OK;
   if (!Wq || !Sx || (!Acc && (!Sw || !Y))) return COMET_ERR_INVALID_ARG;
-  if (Acc == nullptr && (ldy < N)) return COMET_ERR_SHAPE;
+  if (Acc == nullptr && (ldy < N || ldy % 8)) return COMET_ERR_SHAPE;
+  if (Acc == nullptr && ((reinterpret_cast<uintptr_t>(Y) & 15) || (reinterpret_cast<uintptr_t>(Sw) & 15)))
+    return COMET_ERR_ALIGNMENT;
   if ((n8 && !Xq8) || (n4 && !Xq4)) return COMET_ERR_INVALID_ARG;
   if ((n8 && !aligned16(Xq8)) || (n4 && !aligned16(Xq4)) || !aligned16(Wq) || !aligned16(Sx))
     return COMET_ERR_ALIGNMENT;

@@ -82,18 +82,21 @@ def test_c1_tiny_full_parity(mask, group, seed):
     assert_y_close(g["Y"], o["y"], o["y64"])
 
 
-@pytest.mark.parametrize("M", [1, 3, 5, 13, 16, 17, 31, 33, 64, 65, 100, 128, 129, 255, 300])
-def test_ragged_m_all_tile_widths(M):
-    """Every BN specialisation (16/32/64/128) and ragged token tails."""
+@pytest.mark.parametrize("group", [128, 1024])
+@pytest.mark.parametrize("M", [1, 3, 5, 13, 16, 17, 31, 33, 64, 65, 100, 128, 129, 255, 256, 300, 520])
+def test_ragged_m_all_tile_widths(M, group):
+    """Every kernel specialisation (decode BN 16/32/64/128, CTA-pair prefill
+    for M > 128), ragged token tails, N = 384 (a half-populated pair tile),
+    group-128 and per-channel weight scales."""
     p = synth.make_problem(M, 384, 1024, n8=1, seed=100 + M, mask="scattered")
-    g = gpu_path(p, 128, want_acc=True)
-    o = oracle_path(p, 128, want_acc=True)
+    g = gpu_path(p, group, want_acc=True)
+    o = oracle_path(p, group, want_acc=True)
     assert_planes_equal(g, o)
     assert np.array_equal(g["Acc"], o["acc"])
     assert_y_close(g["Y"], o["y"], o["y64"])
 
 
-@pytest.mark.parametrize("M,N,K", [(1, 4096, 4096), (16, 1024, 4096), (8, 512, 8192), (200, 256, 2048)])
+@pytest.mark.parametrize("M,N,K", [(1, 4096, 4096), (16, 1024, 4096), (8, 512, 8192), (128, 256, 2048)])
 def test_split_k_decode_shapes(M, N, K):
     """Few tiles -> split-K with the deterministic last-CTA fixup (a7)."""
     assert comet.comet_w4ax_gemm_workspace_bytes(M, N, K) > 0
@@ -207,19 +210,20 @@ def test_quantize_random_rows_bit_exact_large():
 
 
 # ------------------------------------------------- full-size (sampled) ----
-@pytest.mark.parametrize("M,N,K,n8", [(4096, 11008, 4096, 3), (16, 57344, 8192, 6), (2048, 8192, 28672, 22)])
-def test_full_size_sampled_rows(M, N, K, n8):
+@pytest.mark.parametrize("M,N,K,n8,group", [(4096, 11008, 4096, 3, 128), (4096, 4096, 4096, 3, 4096),
+                                             (16, 57344, 8192, 6, 128), (2048, 8192, 28672, 22, 128)])
+def test_full_size_sampled_rows(M, N, K, n8, group):
     """BJ configs at full size in the launch configuration bench.py times:
     planes/scales bit-exact over ALL rows; INT32 + Y on a 64-row sample."""
     p = synth.make_problem(M, N, K, n8=n8, seed=300)
-    g = gpu_path(p, 128)
+    g = gpu_path(p, group)
     Xq8, Xq4, Sx = oracle.quantize_act(p["X"], p["bits"], p["perm"])
     assert np.array_equal(g["Xq8"], Xq8) and np.array_equal(g["Xq4"], Xq4)
     assert np.array_equal(g["Sx"].view(np.uint32), Sx.view(np.uint32))
-    Wq, Sw = oracle.pack_weight(p["W"], 128, p["perm"])
+    Wq, Sw = oracle.pack_weight(p["W"], group, p["perm"])
     assert np.array_equal(g["Wq"], Wq) and np.array_equal(g["Sw"].view(np.uint32), Sw.view(np.uint32))
     rows = synth.sample_rows(M, 64 if M > 64 else M)
-    r = oracle.w4ax_gemm(Xq8, Xq4, Sx, p["bits"], Wq, Sw, rows=rows, want_y64=True)
+    r = oracle.w4ax_gemm(Xq8, Xq4, Sx, p["bits"], Wq, Sw, group=group, rows=rows, want_y64=True)
     assert_y_close(g["Y"][rows], r["y"], r["y64"])
 
 
