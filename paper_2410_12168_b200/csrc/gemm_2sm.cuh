@@ -7,14 +7,15 @@
 //       INT8 blocks [128 x 128 B] straight into the MMA operand (SW128),
 //       INT4 blocks packed [128 x 64 B]; 1-D bulk copies of the block's scales
 //       into an 8-deep scale ring.
-//   a4  warps 2-3: INT4 -> INT8 zero-extension of the weights (and
-//       of INT4 token blocks) into SW128 K-major smem; then a cluster-scope
-//       arrive on the leader CTA's "expanded" barrier.
+//   a4  warps 2-17 ("compute warps"): INT4 -> INT8 zero-extension
+//       of the weights (and of INT4 token blocks) of block i+1 into SW128
+//       K-major smem -- one 16-byte packed chunk per thread per operand --
+//       then an arrive on the leader CTA's "expanded" barrier ...
 //   a5  warp 1 of the leader CTA: 4 x tcgen05.mma.cta_group::2.kind::i8
 //       (M=256, N=256, K=32) into a fresh INT32 accumulator in both CTAs'
 //       TMEM (two 256-column accumulators ping-pong = all 512 columns);
 //       tcgen05.commit multicasts to both CTAs' barriers.
-//   a6  warps 4-19: tcgen05.ld 16 columns at a time, I2F, and
+//   a6  ... and promote block i: tcgen05.ld 16 columns at a time, I2F, and
 //       y += (sx[m,b] 16^-e_b) * acc  with fma.rn.f32x2 (sx is uniform per
 //       thread because a thread owns a token row); group-128 weights also
 //       multiply by sw[n,b] (mul.rn.f32x2); per-channel weights apply sw[n]
@@ -45,31 +46,13 @@ struct Gemm2Cfg {
   static constexpr int kScaleBytes = kScaleSlots * kSlotBytes + 256 * 4;      // + per-channel sw[256]
   static constexpr int kBarBytes = 256;
   static constexpr int kSmemBytes = kStages * kStageBytes + kScaleBytes + kBarBytes + 1024;
-  static constexpr int kThreads = 640;  // 20 warps
-  static constexpr int kEpiWarp0 = 4;
+  static constexpr int kThreads = 576;  // 18 warps: TMA, MMA, 16 compute
+  static constexpr int kEpiWarp0 = 2;
   static constexpr int kNumEpiWarps = 16;
 };
 
-// Expand `rows` packed rows (64 B) at smem `src` into SW128 int8 rows at
-// `dst` (both shared addresses).  Zero-extension with one LOP3 + one shift +
-// one IADD per 32-bit word:  t = w & 0x0F0F0F0F;  lo = t << 4 (16*e0..3);
-// hi = w - t (16*e4..7).
-DEVI void expand_rows_smem(uint32_t src, uint32_t dst, int rows, int tid, int nthreads) {
-#pragma unroll 4
-  for (int t = tid; t < rows * 4; t += nthreads) {
-    const int r = t >> 2, j = t & 3;
-    const uint4 w = lds128(src + r * 64 + j * 16);
-    const uint32_t t0 = w.x & 0x0F0F0F0Fu, t1 = w.y & 0x0F0F0F0Fu, t2 = w.z & 0x0F0F0F0Fu, t3 = w.w & 0x0F0F0F0Fu;
-    const uint4 o0 = make_uint4(t0 << 4, w.x - t0, t1 << 4, w.y - t1);
-    const uint4 o1 = make_uint4(t2 << 4, w.z - t2, t3 << 4, w.w - t3);
-    const uint32_t row = dst + r * 128;
-    sts128(row + (((2 * j) ^ (r & 7)) << 4), o0);
-    sts128(row + (((2 * j + 1) ^ (r & 7)) << 4), o1);
-  }
-}
-
 template <bool kGroupK, bool kAccOut>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
     w4ax_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX4,
                          const __grid_constant__ CUtensorMap tmX8, const __grid_constant__ BlockMap map, GemmArgs args) {
   using C = Gemm2Cfg;
@@ -109,7 +92,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&expd[s], 4);
+      mbar_init(&expd[s], 2 * C::kNumEpiWarps);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -192,33 +175,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
         __syncwarp();
       }
     }
-  } else if (warp < C::kEpiWarp0) {
-    // ------------------------------------------------ INT4 expansion ----
-    const int tid = threadIdx.x - 64;
-    for (int i = 0; i < nb; ++i) {
-      const int s = i % C::kStages;
-      const uint32_t ph = (i / C::kStages) & 1;
-      const bool is8 = (map.code[i] >> 15) != 0;
-      mbar_wait(&full[s], ph);
-      expand_rows_smem(smem_u32(wp_ptr(s)), b_addr(s), 128, tid, 64);
-      if (!is8) expand_rows_smem(smem_u32(xp_ptr(s)), a_addr(s), 128, tid, 64);
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(leader_expd + s * 8);
-    }
   } else {
-    // ------------------------------------------- promotion epilogue ----
+    // ------------------------------------ compute warps: a4 + a6 + a8 ----
+    // Iteration i: expand block i+1 (INT4 -> INT8 into the stage the MMA
+    // reads next), then promote block i's accumulator.  The MMA of block i+1
+    // overlaps the promotion of block i.
+    const int ct = threadIdx.x - 32 * C::kEpiWarp0;  // 0..511
     const int e = warp - C::kEpiWarp0;
     const int q = warp & 3;            // TMEM lane quarter
     const int cg = e >> 2;             // 64-column group
     const int row = 32 * q + lane;     // token row within this CTA
     const int m = my_m0 + row;
     const uint32_t tl = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(64 * cg);
+    // this thread's expansion task: packed row ct/4, 16-byte chunk ct%4
+    const int er = ct >> 2, ej = ct & 3;
+    const uint32_t e_src = er * 64 + ej * 16;
+    const uint32_t e_dst0 = er * 128 + (((2 * ej) ^ (er & 7)) << 4);
+    const uint32_t e_dst1 = er * 128 + (((2 * ej + 1) ^ (er & 7)) << 4);
+
+    auto expand = [&](int j) {
+      const int s = j % C::kStages;
+      mbar_wait(&full[s], (j / C::kStages) & 1);
+      const uint32_t wp = smem_u32(wp_ptr(s)) + e_src;
+      const uint4 w = lds128(wp);
+      const bool is8 = (map.code[j] >> 15) != 0;
+      uint4 x = make_uint4(0, 0, 0, 0);
+      if (!is8) x = lds128(smem_u32(xp_ptr(s)) + e_src);
+      {
+        const uint32_t t0 = w.x & 0x0F0F0F0Fu, t1 = w.y & 0x0F0F0F0Fu, t2 = w.z & 0x0F0F0F0Fu, t3 = w.w & 0x0F0F0F0Fu;
+        sts128(b_addr(s) + e_dst0, make_uint4(t0 << 4, w.x - t0, t1 << 4, w.y - t1));
+        sts128(b_addr(s) + e_dst1, make_uint4(t2 << 4, w.z - t2, t3 << 4, w.w - t3));
+      }
+      if (!is8) {
+        const uint32_t t0 = x.x & 0x0F0F0F0Fu, t1 = x.y & 0x0F0F0F0Fu, t2 = x.z & 0x0F0F0F0Fu, t3 = x.w & 0x0F0F0F0Fu;
+        sts128(a_addr(s) + e_dst0, make_uint4(t0 << 4, x.x - t0, t1 << 4, x.y - t1));
+        sts128(a_addr(s) + e_dst1, make_uint4(t2 << 4, x.z - t2, t3 << 4, x.w - t3));
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_expd + s * 8);
+    };
+
     float2 y[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) y[j] = make_float2(0.f, 0.f);
 
+    expand(0);
     for (int i = 0; i < nb; ++i) {
+      if (i + 1 < nb) expand(i + 1);
       const int acc = i & 1;
       const uint32_t aph = (i >> 1) & 1;
       const int a = i % C::kScaleSlots;

@@ -167,9 +167,13 @@ DEVI uint32_t mapa_shared(uint32_t local_addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
   return r;
 }
-// arrive (release, cluster scope) on an mbarrier given by its shared::cluster address
+// arrive on an mbarrier given by its shared::cluster address (possibly in the
+// peer CTA).  Default .release.cta semantics, as CUTLASS's ClusterBarrier:
+// compiles to a bare SYNCS.ARRIVE (a .release.cluster arrive costs a
+// MEMBAR.ALL.GPU per call).  Producers of smem operands issue
+// fence.proxy.async before it.
 DEVI void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 DEVI bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
