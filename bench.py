@@ -5,7 +5,8 @@
 
 Workload (default, BASELINE.json configs[1]): LLaMA-2-7B linear shapes,
 K=4096, N in {4096, 11008}, M=4096 tokens (the top of the M=1..4096 range),
-3/32 INT8 blocks (~10%), group-128 INT4 weights, seeded synthetic inputs
+3/32 INT8 blocks (~10%), INT4 weights with per-output-channel scales
+(--group 128 for 128-channel groups), seeded synthetic inputs
 (paper_2410_12168_b200.synth).  One step = one pass of the hot path over
 both layers: quantize_act (a1+a2) + w4ax_gemm (a3..a8) per layer
 (+ the NCCL all-gather of Y when N>1: weights N-sharded, X replicated).
@@ -36,7 +37,7 @@ METRIC = "W4Ax GEMM TOPS & % of B200 INT8/HBM roofline; linear-layer tokens/s at
 
 CONFIGS = {
     # BASELINE.json configs[1]
-    "llama2-7b": dict(workload="LLaMA-2-7B linear shapes (K=4096, N=4096/11008), M=4096, 3/32 INT8 blocks, g=128",
+    "llama2-7b": dict(workload="LLaMA-2-7B linear shapes (K=4096, N=4096/11008), M=4096, 3/32 INT8 blocks",
                       M=4096, layers=[(4096, 4096), (11008, 4096)], n8=[3, 3]),
     # decode point of the same config
     "llama2-7b-decode": dict(workload="LLaMA-2-7B linear shapes (K=4096, N=4096/11008), M=16 decode, 3/32 INT8 blocks",
@@ -149,13 +150,14 @@ def run_reference(args, cfg):
     layers = []
     for li, ((N, K), n8) in enumerate(zip(cfg["layers"], cfg["n8"])):
         p = synth.make_problem(M, N, K, n8=n8, seed=100 + li, x_rows=rows)
-        Wq, Sw = oracle.pack_weight(p["W"], 128, p["perm"])
-        layers.append((p, Wq, Sw))
+        g = group_of(args, K)
+        Wq, Sw = oracle.pack_weight(p["W"], g, p["perm"])
+        layers.append((p, Wq, Sw, g))
 
     def step():
-        for p, Wq, Sw in layers:
+        for p, Wq, Sw, g in layers:
             Xq8, Xq4, Sx = oracle.quantize_act(p["X"], p["bits"], p["perm"])
-            oracle.w4ax_gemm(Xq8, Xq4, Sx, p["bits"], Wq, Sw, group=128)
+            oracle.w4ax_gemm(Xq8, Xq4, Sx, p["bits"], Wq, Sw, group=g)
 
     for _ in range(args.warmup):
         step()
@@ -170,7 +172,7 @@ def run_reference(args, cfg):
     out = {"impl": "reference", "metric": METRIC, "value": tops, "unit": "TOPS", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "int8/int32+f64", "data": "synthetic",
-           "config": {"workload": cfg["workload"], "M": M, "layers": cfg["layers"]},
+           "config": {"workload": cfg["workload"], "M": M, "layers": cfg["layers"], "weight_scales": args.group},
            "tokens_per_s": len(rows) / dt,
            "cpu_baseline": {"value": tops, "unit": "TOPS", "cores": cores, "kind": "oracle", "sample": sample},
            "e2e": {"value": tops, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -178,7 +180,12 @@ def run_reference(args, cfg):
     return 0
 
 
-def cpu_baseline(cfg, seconds_target=10.0):
+def group_of(args, K):
+    """weight-scale group size: K (per output channel) or 128"""
+    return K if args.group == "channel" else 128
+
+
+def cpu_baseline(cfg, args, seconds_target=10.0):
     """Oracle timed on the host cores on a bounded row sample (rank 0, N=1)."""
     import oracle
     from paper_2410_12168_b200 import synth
@@ -188,14 +195,15 @@ def cpu_baseline(cfg, seconds_target=10.0):
     layers = []
     for li, ((N, K), n8) in enumerate(zip(cfg["layers"], cfg["n8"])):
         p = synth.make_problem(M, N, K, n8=n8, seed=100 + li, x_rows=rows)
-        Wq, Sw = oracle.pack_weight(p["W"], 128, p["perm"])
-        layers.append((p, Wq, Sw))
+        g = group_of(args, K)
+        Wq, Sw = oracle.pack_weight(p["W"], g, p["perm"])
+        layers.append((p, Wq, Sw, g))
     t0 = time.perf_counter()
     reps = 0
     while True:
-        for p, Wq, Sw in layers:
+        for p, Wq, Sw, g in layers:
             Xq8, Xq4, Sx = oracle.quantize_act(p["X"], p["bits"], p["perm"])
-            oracle.w4ax_gemm(Xq8, Xq4, Sx, p["bits"], Wq, Sw, group=128)
+            oracle.w4ax_gemm(Xq8, Xq4, Sx, p["bits"], Wq, Sw, group=g)
         reps += 1
         if time.perf_counter() - t0 > seconds_target or reps >= 50:
             break
@@ -230,8 +238,9 @@ def run_comet(args, cfg, config_name):
         perm = torch.from_numpy(p["perm"]).to(dev)
         bits = comet.BlockBits(p["bits"])
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        grp = group_of(args, K)
         e0.record()
-        Wq, Sw = comet.comet_pack_weight(W, perm, 128)
+        Wq, Sw = comet.comet_pack_weight(W, perm, grp)
         e1.record()
         torch.cuda.synchronize()
         t_pack += e0.elapsed_time(e1)
@@ -243,7 +252,7 @@ def run_comet(args, cfg, config_name):
         Xh = torch.from_numpy(p["X"]).pin_memory()
         Yh = torch.empty((M, per), dtype=torch.float16).pin_memory()
         scratch = comet.new_workspace(comet.comet_w4ax_linear_scratch_bytes(M, per, K, bits), dev)
-        layers.append(dict(N=N, K=K, per=per, W=W, perm=perm, bits=bits, Wq=Wq, Sw=Sw, X=X, planes=planes, Y=Y,
+        layers.append(dict(N=N, K=K, grp=grp, per=per, W=W, perm=perm, bits=bits, Wq=Wq, Sw=Sw, X=X, planes=planes, Y=Y,
                            ws=ws, Yall=Yall, Xh=Xh, Yh=Yh, scratch=scratch, ev=[]))
         del p
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
@@ -254,7 +263,7 @@ def run_comet(args, cfg, config_name):
             if timed_kernels:
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-            comet.comet_w4ax_gemm(Xq8, Xq4, Sx, L["bits"], L["Wq"], L["Sw"], 128, out=L["Y"], workspace=L["ws"])
+            comet.comet_w4ax_gemm(Xq8, Xq4, Sx, L["bits"], L["Wq"], L["Sw"], L["grp"], out=L["Y"], workspace=L["ws"])
             if timed_kernels:
                 b.record(stream)
                 L["ev"].append((a, b))
@@ -295,7 +304,7 @@ def run_comet(args, cfg, config_name):
         barrier()
         t0 = time.perf_counter()
         for L in layers:
-            comet.comet_w4ax_linear(L["Xh"], L["bits"], L["Wq"], L["Sw"], perm=L["perm"], out=L["Yh"],
+            comet.comet_w4ax_linear(L["Xh"], L["bits"], L["Wq"], L["Sw"], perm=L["perm"], group=L["grp"], out=L["Yh"],
                                     scratch=L["scratch"])
         torch.cuda.synchronize()
         if it >= args.warmup:
@@ -320,7 +329,7 @@ def run_comet(args, cfg, config_name):
     ops_d = 2.0 * M * Ld["per"] * Ld["K"]
     nb = Ld["K"] // 128
     n8 = Ld["bits"].n8
-    bytes_d = (Ld["per"] * Ld["K"] / 2 + 4 * Ld["per"] * nb + M * (128 * n8 + 64 * (nb - n8)) + 4 * M * nb
+    bytes_d = (Ld["per"] * Ld["K"] / 2 + 4 * Ld["per"] * (Ld["K"] // Ld["grp"]) + M * (128 * n8 + 64 * (nb - n8)) + 4 * M * nb
                + 2 * M * Ld["per"])
     int8_peak = 2.0 * peaks["bf16_tflops"]  # dense int8 = 2x bf16 (nominal 4.5 vs 2.25 PF)
     t_tc = ops_d / (int8_peak * 1e12)
@@ -342,7 +351,7 @@ def run_comet(args, cfg, config_name):
            "warmup": args.warmup, "ms_per_step": t_dev, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "int8 (INT4/INT8 operands) x int32 accum, fp32 dequant, fp16 out",
            "data": "synthetic (seeded; X~N(0,1) + planted outlier channels, W~N(0,1/K))",
-           "config": {"workload": cfg["workload"], "M": M, "layers": cfg["layers"], "group": 128,
+           "config": {"workload": cfg["workload"], "M": M, "layers": cfg["layers"], "weight_scales": args.group,
                       "parallelism": f"tp{world} (N-sharded, NCCL all-gather of Y)" if world > 1 else "single GPU",
                       "l2": "flushed (256 MiB write) before every timed step, outside the events"},
            "tokens_per_s": M / (t_dev * 1e-3),
@@ -354,7 +363,7 @@ def run_comet(args, cfg, config_name):
            "roofline": roof,
            "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(cfg, seconds_target=args.cpu_seconds)
+        out["cpu_baseline"] = cpu_baseline(cfg, args, seconds_target=args.cpu_seconds)
     if rank == 0:
         print(json.dumps(out))
     if world > 1:
@@ -371,6 +380,8 @@ def main():
     ap.add_argument("--impl", default="comet", choices=["comet", "reference"])
     ap.add_argument("--config", default="llama2-7b", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--group", default="channel", choices=["channel", "128"],
+                    help="weight-scale granularity: per output channel (OmniQuant W4A4 style, default) or 128-groups")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]

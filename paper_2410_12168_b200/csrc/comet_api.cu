@@ -108,7 +108,8 @@ bool build_block_map(const uint8_t* bits, int nb, BlockMap* map, int* n8, int* n
 // ---- GEMM launch plan -----------------------------------------------------
 struct Plan {
   int bn, m_tiles, n_tiles, splits;
-  bool two_sm;  // prefill: CTA-pair kernel (256 tokens x 256 weight rows per pair)
+  bool two_sm;   // prefill: CTA-pair kernel (256 tokens x 256 weight rows per pair)
+  int clusters;  // persistent CTA pairs
   int64_t ws_bytes;
 };
 constexpr int64_t kCounterBytes = 64 * 1024;
@@ -122,8 +123,10 @@ Plan make_plan(int M, int N, int K, int num_sms) {
     p.n_tiles = (N + 255) / 256;
     p.splits = 1;
     p.ws_bytes = 0;
+    p.clusters = num_sms / 2;
     return p;
   }
+  p.clusters = 0;
   p.bn = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128;
   p.m_tiles = (M + p.bn - 1) / p.bn;
   p.n_tiles = N / 128;
@@ -165,8 +168,13 @@ comet_status launch_gemm_2sm(const CUtensorMap& tmW, const CUtensorMap& tmX4, co
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes); });
   if (attr_err != cudaSuccess) return cuda_fail(attr_err);
-  dim3 grid(2 * p.m_tiles, p.n_tiles, 1);
-  kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(tmW, tmX4, tmX8, map, args);
+  PairSched sched;
+  sched.m_tiles = p.m_tiles;
+  sched.n_tiles = p.n_tiles;
+  sched.tiles = p.m_tiles * p.n_tiles;
+  sched.clusters = sched.tiles < p.clusters ? sched.tiles : p.clusters;  // persistent: one cluster per SM pair
+  dim3 grid(2 * sched.clusters, 1, 1);
+  kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(tmW, tmX4, tmX8, map, args, sched);
   return check_launch();
 }
 

@@ -267,4 +267,29 @@ DEVI float2 mul2(float2 a, float2 b) {
 }
 DEVI float i2f(uint32_t v) { return __int2float_rn((int32_t)v); }
 
+// y += (float(a0), float(a1)) * s  -- two I2F into an aligned register pair
+// and one FFMA2, in one asm block so no pair-forming moves are needed.
+DEVI void cvt_fma2(uint64_t& y, uint32_t a0, uint32_t a1, uint64_t s) {
+  asm("{\n .reg .f32 lo, hi;\n .reg .b64 p;\n"
+      " cvt.rn.f32.s32 lo, %1;\n cvt.rn.f32.s32 hi, %2;\n mov.b64 p, {lo, hi};\n"
+      " fma.rn.f32x2 %0, p, %3, %0;\n}\n"
+      : "+l"(y)
+      : "r"(a0), "r"(a1), "l"(s));
+}
+DEVI uint64_t pack2(float lo, float hi) {
+  uint64_t p;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(p) : "f"(lo), "f"(hi));
+  return p;
+}
+DEVI uint64_t mul2_u(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+DEVI float2 unpack2(uint64_t p) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(p));
+  return make_float2(lo, hi);
+}
+
 }  // namespace comet
