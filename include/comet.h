@@ -43,7 +43,13 @@
  *       as int8 ("zero extension ... multiplied by 16").
  *   Sx  fp32 [K/128 x ldsx], Sx[b*ldsx + m] = scale of row m, block b;
  *       ldsx >= M, ldsx % 4 == 0; entries m in [M, ldsx) are written as 1.0.
- *   Wq  packed INT4 [N x K/2 bytes], same nibble order, K on the permuted axis.
+ *   Wq  packed INT4, N*K/2 bytes, same nibble order, K on the permuted axis,
+ *       TILED for contiguous streaming (the B200 counterpart of the paper's
+ *       offline weight interleave): the slab of output channels
+ *       [128*t, 128*t+128) x K-block b (128 rows x 64 bytes) is contiguous at
+ *       byte offset (t*(K/128) + b)*8192; inside it, 16-byte chunk c
+ *       (channels 32c..32c+31 of the block) of row r is stored at byte
+ *       r*64 + ((c ^ ((r >> 1) & 3)) << 4).  Requires N % 128 == 0.
  *   Sw  fp32 [K/group x N], Sw[j*N + n] = scale of output channel n, group j.
  *   Y   fp16 [M x N], row stride ldy elements (ldy >= N, ldy % 8 == 0).
  * Quantization (all blocks, weights and activations): symmetric absmax,
@@ -84,8 +90,8 @@ int64_t comet_w4ax_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K);
 int64_t comet_w4ax_linear_scratch_bytes(int32_t M, int32_t N, int32_t K, const uint8_t* block_bits);
 
 /* ---- a0: offline weight preparation -------------------
- * W fp16 [N x K] (row stride ldw) -> Wq packed INT4 [N x K/2], Sw fp32
- * [K/group x N].  The K axis is permuted by `perm` first (weights are
+ * W fp16 [N x K] (row stride ldw) -> Wq packed INT4 (tiled layout above),
+ * Sw fp32 [K/group x N].  N % 128 == 0.  The K axis is permuted by `perm` first (weights are
  * permuted like the activations), then quantized per (n, group of
  * `group` consecutive permuted channels), group in {128, K}. */
 comet_status comet_pack_weight(const void* W, int64_t ldw, int32_t N, int32_t K, const int32_t* perm,

@@ -113,6 +113,21 @@ def launch_count() -> int:
     return int(lib().comet_launch_count())
 
 
+# ---------------------------------------------------------------- layout ----
+def wq_tiled_to_rowmajor(wq_tiled: np.ndarray, N: int, K: int) -> np.ndarray:
+    """Tiled packed weights (include/comet.h) -> row-major [N x K/2] bytes.
+
+    Pure data movement (no arithmetic of the method): slab (n//128, k-block b)
+    of 128 rows x 64 B is contiguous; 16-B chunk c of row r sits at chunk
+    c ^ ((r >> 1) & 3)."""
+    nb = K // BLOCK
+    t = np.asarray(wq_tiled, dtype=np.uint8).reshape(N // 128, nb, 128, 4, 16)
+    r = np.arange(128)[:, None]
+    c = np.arange(4)[None, :]
+    t = t[:, :, r, c ^ ((r >> 1) & 3), :]             # undo the chunk swizzle
+    return np.ascontiguousarray(t.transpose(0, 2, 1, 3, 4).reshape(N, K // 2))
+
+
 # ----------------------------------------------------------------- sizes ----
 def comet_act_ldsx(M: int) -> int:
     return int(lib().comet_act_ldsx(M))
@@ -135,7 +150,8 @@ def new_workspace(nbytes: int, device) -> Optional[torch.Tensor]:
 
 # -------------------------------------------------------------- entries ----
 def comet_pack_weight(W: torch.Tensor, perm: Optional[torch.Tensor] = None, group: int = BLOCK, stream=None):
-    """a0: W fp16 [N x K] -> (Wq uint8 [N x K/2], Sw fp32 [K/group x N])."""
+    """a0: W fp16 [N x K] -> (Wq uint8 [N x K/2] bytes in the TILED layout,
+    Sw fp32 [K/group x N]); see wq_tiled_to_rowmajor."""
     assert W.is_cuda and W.dtype == torch.float16 and W.dim() == 2 and W.stride(1) == 1
     N, K = W.shape
     Wq = torch.empty((N, K // 2), dtype=torch.uint8, device=W.device)

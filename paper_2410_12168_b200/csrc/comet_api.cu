@@ -12,6 +12,7 @@
 #include "../../include/comet.h"
 #include "gemm.cuh"
 #include "gemm_2sm.cuh"
+#include "gemm_decode.cuh"
 #include "quantize.cuh"
 
 using namespace comet;
@@ -117,46 +118,25 @@ constexpr int64_t kCounterBytes = 64 * 1024;
 Plan make_plan(int M, int N, int K, int num_sms) {
   Plan p;
   p.two_sm = M > 128;
+  p.splits = 1;
   if (p.two_sm) {
     p.bn = 128;  // token rows per CTA (TMA box height)
     p.m_tiles = (M + 255) / 256;
     p.n_tiles = (N + 255) / 256;
-    p.splits = 1;
     p.ws_bytes = 0;
     p.clusters = num_sms / 2;
     return p;
   }
-  p.clusters = 0;
+  // decode: stream-K over (tile, K-block) units, one CTA per SM
   p.bn = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128;
   p.m_tiles = (M + p.bn - 1) / p.bn;
   p.n_tiles = N / 128;
-  const int nb = K / 128;
-  const int tiles = p.m_tiles * p.n_tiles;
-  const int ctas_per_sm = p.bn <= 64 ? 2 : 1;
-  const int target = num_sms * ctas_per_sm;
-  p.splits = 1;
-  if (tiles > 0 && tiles < target) {
-    int s = (target + tiles / 2) / tiles;
-    int max_s = nb / 2 > 1 ? nb / 2 : 1;  // keep >= 2 blocks per split
-    p.splits = s < 1 ? 1 : (s > max_s ? max_s : s);
-    if (tiles > kCounterBytes / 4) p.splits = 1;
-  }
-  p.ws_bytes = p.splits > 1 ? kCounterBytes + (int64_t)tiles * p.splits * p.bn * 128 * 4 : 0;
+  const int64_t tiles = (int64_t)p.m_tiles * p.n_tiles;
+  const int64_t units = tiles * (K / 128);
+  p.clusters = (int)(units < num_sms ? units : num_sms);  // CTAs
+  p.ws_bytes = kCounterBytes + (int64_t)p.clusters * 2 * 128 * p.bn * 4;
+  if (tiles > kCounterBytes / 4) p.ws_bytes = -1;  // more tiles than tile counters
   return p;
-}
-
-template <int BN, bool kAcc>
-comet_status launch_gemm_bn(const CUtensorMap& tmW, const CUtensorMap& tmX4, const CUtensorMap& tmX8,
-                            const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
-  using C = GemmCfg<BN>;
-  auto kern = w4ax_gemm_kernel<BN, kAcc>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes); });
-  if (attr_err != cudaSuccess) return cuda_fail(attr_err);
-  dim3 grid(p.n_tiles, p.m_tiles, p.splits);
-  kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(tmW, tmX4, tmX8, map, args);
-  return check_launch();
 }
 
 template <bool kGroupK, bool kAcc>
@@ -178,19 +158,45 @@ comet_status launch_gemm_2sm(const CUtensorMap& tmW, const CUtensorMap& tmX4, co
   return check_launch();
 }
 
+template <int BN, bool kGroupK, bool kAcc>
+comet_status launch_decode(const CUtensorMap& tmW, const CUtensorMap& tmX4, const CUtensorMap& tmX8,
+                           const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
+  using C = DecCfg<BN>;
+  auto kern = w4ax_gemm_decode_kernel<BN, kGroupK, kAcc>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes); });
+  if (attr_err != cudaSuccess) return cuda_fail(attr_err);
+  DecSched sched;
+  sched.n_tiles = p.n_tiles;
+  sched.tiles = p.n_tiles * p.m_tiles;
+  sched.units = sched.tiles * args.nb;
+  sched.ctas = p.clusters;
+  kern<<<sched.ctas, C::kThreads, C::kSmemBytes, st>>>(tmW, tmX4, tmX8, map, args, sched);
+  return check_launch();
+}
+
+template <bool kGroupK, bool kAcc>
+comet_status launch_decode_bn(const CUtensorMap& tmW, const CUtensorMap& tmX4, const CUtensorMap& tmX8,
+                              const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
+  switch (p.bn) {
+    case 16: return launch_decode<16, kGroupK, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
+    case 32: return launch_decode<32, kGroupK, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
+    case 64: return launch_decode<64, kGroupK, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
+    default: return launch_decode<128, kGroupK, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
+  }
+}
+
 template <bool kAcc>
 comet_status launch_gemm(const CUtensorMap& tmW, const CUtensorMap& tmX4, const CUtensorMap& tmX8,
                          const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
+  const bool group_k = args.group_blocks == args.nb;
   if (p.two_sm) {
-    if (args.group_blocks == args.nb) return launch_gemm_2sm<true, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
+    if (group_k) return launch_gemm_2sm<true, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
     return launch_gemm_2sm<false, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
   }
-  switch (p.bn) {
-    case 16: return launch_gemm_bn<16, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
-    case 32: return launch_gemm_bn<32, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
-    case 64: return launch_gemm_bn<64, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
-    default: return launch_gemm_bn<128, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
-  }
+  if (group_k) return launch_decode_bn<true, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
+  return launch_decode_bn<false, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
 }
 
 comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx, const uint8_t* bits,
@@ -216,9 +222,12 @@ comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, in
   comet_status ds = device_check(&num_sms);
   if (ds != COMET_OK) return ds;
   Plan p = make_plan(M, N, K, num_sms);
+  if (p.ws_bytes < 0) return COMET_ERR_SHAPE;
   if (!Acc && p.ws_bytes > 0 && (ws == nullptr || (int64_t)ws_bytes < p.ws_bytes)) return COMET_ERR_WORKSPACE;
 
   CUtensorMap tmW, tmX4, tmX8;
+  // weights are tiled (8 KB contiguous slabs) and loaded with 1-D bulk copies;
+  // tmW is an unused placeholder map
   if (!make_map_u8(&tmW, Wq, (uint64_t)K / 2, (uint64_t)N, (uint64_t)K / 2, 64, 128, CU_TENSOR_MAP_SWIZZLE_NONE))
     return COMET_ERR_CUDA;
   if (n4) {
@@ -246,6 +255,7 @@ comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, in
   a.Sw = Sw;
   a.group_blocks = group / 128;
   a.Y = reinterpret_cast<__half*>(Y);
+  a.Wq = reinterpret_cast<const uint8_t*>(Wq);
   a.Acc = Acc;
   a.splits = p.splits;
   a.ws_counter = reinterpret_cast<int*>(ws);
@@ -294,7 +304,7 @@ int64_t comet_w4ax_linear_scratch_bytes(int32_t M, int32_t N, int32_t K, const u
 comet_status comet_pack_weight(const void* W, int64_t ldw, int32_t N, int32_t K, const int32_t* perm, int32_t group,
                                void* Wq, float* Sw, comet_stream_t stream) {
   if (N < 0 || K <= 0) return COMET_ERR_INVALID_ARG;
-  if (K % 128 || K > 65536 || (group != 128 && group != K) || ldw < K || ldw % 8) return COMET_ERR_SHAPE;
+  if (K % 128 || K > 65536 || N % 128 || (group != 128 && group != K) || ldw < K || ldw % 8) return COMET_ERR_SHAPE;
   if (N == 0) return COMET_OK;
   if (!W || !Wq || !Sw) return COMET_ERR_INVALID_ARG;
   if (!aligned16(W) || !aligned16(Wq) || (perm && !aligned16(perm))) return COMET_ERR_ALIGNMENT;
@@ -311,11 +321,11 @@ comet_status comet_pack_weight(const void* W, int64_t ldw, int32_t N, int32_t K,
     if (grid > 148 * 16) grid = 148 * 16;
     // Sw layout [K/128 x N] is the Sx layout with ldsx == N (no padding rows)
     if (perm)
-      quantize_act_kernel<true><<<grid, 256, 0, st>>>(Wh, ldw, N, K / 128, N, perm, map, nullptr, 0,
-                                                       reinterpret_cast<uint8_t*>(Wq), K / 2, Sw);
+      quantize_act_kernel<true, true><<<grid, 256, 0, st>>>(Wh, ldw, N, K / 128, N, perm, map, nullptr, 0,
+                                                             reinterpret_cast<uint8_t*>(Wq), K / 2, Sw);
     else
-      quantize_act_kernel<false><<<grid, 256, 0, st>>>(Wh, ldw, N, K / 128, N, perm, map, nullptr, 0,
-                                                        reinterpret_cast<uint8_t*>(Wq), K / 2, Sw);
+      quantize_act_kernel<false, true><<<grid, 256, 0, st>>>(Wh, ldw, N, K / 128, N, perm, map, nullptr, 0,
+                                                              reinterpret_cast<uint8_t*>(Wq), K / 2, Sw);
   } else {
     int grid = (N + 7) / 8;
     if (perm)
@@ -449,6 +459,18 @@ const char* comet_status_str(comet_status s) {
 }
 
 const char* comet_last_cuda_error(void) { return g_cuda_err; }
+
+// debug only (not part of comet.h): enable/read per-CTA timestamps of the
+// decode kernel, [start_ns, end_ns, smid] x n
+int comet_debug_cta_times(int enable, unsigned long long* host, int n) {
+  int on = enable;
+  if (cudaMemcpyToSymbol(g_cta_times_on, &on, sizeof(int)) != cudaSuccess) return -1;
+  if (host && n > 0) {
+    if (n > 1024) n = 1024;
+    if (cudaMemcpyFromSymbol(host, g_cta_times, sizeof(unsigned long long) * 3 * n) != cudaSuccess) return -1;
+  }
+  return 0;
+}
 int64_t comet_launch_count(void) { return g_launches.load(); }
 
 }  // extern "C"

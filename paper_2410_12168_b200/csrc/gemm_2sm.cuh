@@ -11,7 +11,8 @@
 // re-fill between tiles and one sync per tile before write-back.
 //
 // Per block and CTA:
-//   a3  warp 16: TMA the packed weight slab [128 x 64 B] and the token slab
+//   a3  warp 16: 1-D bulk copy of the packed weight slab [128 x 64 B] (tiled
+//       weight layout) and TMA of the token slab
 //       (INT8 blocks [128 x 128 B] straight into the MMA operand with
 //       128B swizzle, INT4 blocks packed [128 x 64 B]); 1-D bulk copies of
 //       the block's scales into an 8-deep scale ring.
@@ -66,10 +67,23 @@ struct PairSched {
   }
 };
 
+// Zero-extension of one packed word w: t = w & 0x0F0F0F0F (LOP3,
+// ALU pipe), lo = 16*t = 16*e0..3 and hi = w - t = 16*e4..7 as IMADs (FMA
+// pipe) -- the ALU pipe is shared with I2F in the promotion.
+DEVI void zext_word(uint32_t w, uint32_t& lo, uint32_t& hi) {
+  uint32_t t;
+  asm("and.b32 %0, %1, 0x0F0F0F0F;" : "=r"(t) : "r"(w));
+  asm("mul.lo.u32 %0, %1, 16;" : "=r"(lo) : "r"(t));
+  asm("mad.lo.u32 %0, %1, 0xFFFFFFFF, %2;" : "=r"(hi) : "r"(t), "r"(w));
+}
 DEVI void expand_chunk(uint4 w, uint32_t dst0, uint32_t dst1) {
-  const uint32_t t0 = w.x & 0x0F0F0F0Fu, t1 = w.y & 0x0F0F0F0Fu, t2 = w.z & 0x0F0F0F0Fu, t3 = w.w & 0x0F0F0F0Fu;
-  sts128(dst0, make_uint4(t0 << 4, w.x - t0, t1 << 4, w.y - t1));  // 16*e0..3 | 16*e4..7
-  sts128(dst1, make_uint4(t2 << 4, w.z - t2, t3 << 4, w.w - t3));
+  uint4 o0, o1;
+  zext_word(w.x, o0.x, o0.y);
+  zext_word(w.y, o0.z, o0.w);
+  zext_word(w.z, o1.x, o1.y);
+  zext_word(w.w, o1.z, o1.w);
+  sts128(dst0, o0);  // 16*e0..3 | 16*e4..7 of words 0,1
+  sts128(dst1, o1);
 }
 
 template <bool kGroupK, bool kAccOut>
@@ -143,8 +157,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
       mbar_wait(&empty[s], ((g / C::kStages) & 1) ^ 1);
       uint8_t* st = smem + s * C::kStageBytes;
       if (elect_one()) {
-        mbar_arrive_expect_tx(&full[s], C::kWPBytes + (is8 ? C::kABytes : C::kXPBytes));
-        tma_load_2d(st + C::kABytes + C::kBBytes + C::kXPBytes, &tmW, &full[s], b * 64, n0 + 128 * (int)crank);
+        // a half-populated pair tile (N % 256 == 128): the second CTA's weight
+        // rows are past N -- no load; its (unused) output columns are never stored
+        const bool w_valid = n0 + 128 * (int)crank < args.N;
+        mbar_arrive_expect_tx(&full[s], (w_valid ? C::kWPBytes : 0) + (is8 ? C::kABytes : C::kXPBytes));
+        if (w_valid)
+          bulk_load(st + C::kABytes + C::kBBytes + C::kXPBytes,
+                    args.Wq + ((int64_t)((n0 >> 7) + (int)crank) * nb + b) * 8192, 8192, &full[s]);
         if (is8)
           tma_load_2d(st, &tmX8, &full[s], rank * 128, my_m0);
         else
@@ -214,10 +233,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
       const uint32_t st = sbase + s * C::kStageBytes;
       const int er = ct >> 2, ej = ct & 3;
       const uint32_t e_src = er * 64 + ej * 16;
+      const uint32_t w_src = er * 64 + ((ej ^ ((er >> 1) & 3)) << 4);  // tiled weights: 64B swizzle
       const uint32_t e_dst0 = er * 128 + (((2 * ej) ^ (er & 7)) << 4);
       const uint32_t e_dst1 = er * 128 + (((2 * ej + 1) ^ (er & 7)) << 4);
       mbar_wait(&full[s], (j / C::kStages) & 1);
-      const uint4 w = lds128(st + C::kABytes + C::kBBytes + C::kXPBytes + e_src);
+      const uint4 w = lds128(st + C::kABytes + C::kBBytes + C::kXPBytes + w_src);
       if (!is8) {
         const uint4 x = lds128(st + C::kABytes + C::kBBytes + e_src);
         expand_chunk(x, st + e_dst0, st + e_dst1);

@@ -68,8 +68,18 @@ DEVI void load_octet(const __half* __restrict__ X, int64_t ldx, int64_t m, int b
   }
 }
 
+// Byte offset of packed byte p (0 <= p < K/2) of weight row n in the tiled
+// weight layout (include/comet.h): slab (n/128, p/64) of 128 rows x 64 B is
+// contiguous, 16-B chunk c of row r stored at chunk c ^ ((r >> 1) & 3).
+DEVI int64_t wq_tiled_offset(int64_t n, int64_t p, int nb) {
+  const int64_t tile = n >> 7, r = n & 127, kb = p >> 6, c = (p >> 4) & 3, j = p & 15;
+  return ((tile * nb + kb) * 128 + r) * 64 + ((c ^ ((r >> 1) & 3)) << 4) + j;
+}
+
 // Activation quantize + pack.  rows = ldsx (rows >= M get only Sx = 1.0).
-template <bool kPerm>
+// kTiledW: the INT4 plane is a weight matrix written in the tiled layout
+// (comet_pack_weight, group 128).
+template <bool kPerm, bool kTiledW = false>
 __global__ void __launch_bounds__(256) quantize_act_kernel(const __half* __restrict__ X, int64_t ldx, int M, int nb,
                                                            int64_t ldsx, const int32_t* __restrict__ perm,
                                                            const __grid_constant__ BlockMap map, int8_t* __restrict__ Xq8,
@@ -114,6 +124,8 @@ __global__ void __launch_bounds__(256) quantize_act_kernel(const __half* __restr
       uint32_t hi = (uint32_t)(q[4] & 0xFF) | ((uint32_t)(q[5] & 0xFF) << 8) | ((uint32_t)(q[6] & 0xFF) << 16) |
                     ((uint32_t)(q[7] & 0xFF) << 24);
       *reinterpret_cast<uint2*>(Xq8 + m * ld8 + (int64_t)rank * 128 + o * 8) = make_uint2(lo, hi);
+    } else if (kTiledW) {
+      *reinterpret_cast<uint32_t*>(Xq4 + wq_tiled_offset(m, (int64_t)rank * 64 + o * 4, nb)) = pack_int4_word(q);
     } else {
       *reinterpret_cast<uint32_t*>(Xq4 + m * ld4 + (int64_t)rank * 64 + o * 4) = pack_int4_word(q);
     }
@@ -122,7 +134,8 @@ __global__ void __launch_bounds__(256) quantize_act_kernel(const __half* __restr
 }
 
 // Weight pack with one scale per output channel (group == K): a warp per
-// row, pass 1 = absmax over the permuted row, pass 2 = quantize + pack.
+// row, pass 1 = absmax over the permuted row, pass 2 = quantize + pack
+// (tiled weight layout).
 template <bool kPerm>
 __global__ void __launch_bounds__(256) pack_weight_rowscale_kernel(const __half* __restrict__ W, int64_t ldw, int N,
                                                                    int K, const int32_t* __restrict__ perm,
@@ -150,7 +163,7 @@ __global__ void __launch_bounds__(256) pack_weight_rowscale_kernel(const __half*
     load_octet<kPerm>(W, ldw, n, t >> 4, t & 15, perm, x);
     int32_t q[8];
     quant8(x, r, q);
-    *reinterpret_cast<uint32_t*>(Wq + n * (K / 2) + (int64_t)t * 4) = pack_int4_word(q);
+    *reinterpret_cast<uint32_t*>(Wq + wq_tiled_offset(n, (int64_t)t * 4, K / 128)) = pack_int4_word(q);
   }
   if (lane == 0) Sw[n] = s;
 }

@@ -227,6 +227,14 @@ DEVI void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* 
       : "memory");
 }
 
+DEVI void bulk_load_hint(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
 // ------------------------------------------------------------ smem I/O ----
 DEVI uint4 lds128(uint32_t addr) {
   uint4 v;
@@ -276,6 +284,17 @@ DEVI void cvt_fma2(uint64_t& y, uint32_t a0, uint32_t a1, uint64_t s) {
       : "+l"(y)
       : "r"(a0), "r"(a1), "l"(s));
 }
+// Same result via the exact magic-number conversion on the FMA pipe:
+// asfloat(0x4B400000 + a) = 1.5*2^23 + a exactly for |a| < 2^22, so
+// (asfloat(0x4B400000 + a) - 1.5*2^23) == float(a) with no rounding.
+DEVI void cvt_fma2_magic(uint64_t& y, uint32_t a0, uint32_t a1, uint64_t s) {
+  asm("{\n .reg .b32 lo, hi;\n .reg .b64 p;\n"
+      " mad.lo.u32 lo, %1, 1, 0x4B400000;\n mad.lo.u32 hi, %2, 1, 0x4B400000;\n mov.b64 p, {lo, hi};\n"
+      " add.rn.f32x2 p, p, %4;\n"
+      " fma.rn.f32x2 %0, p, %3, %0;\n}\n"
+      : "+l"(y)
+      : "r"(a0), "r"(a1), "l"(s), "l"(0xCB400000CB400000ull));
+}
 DEVI uint64_t pack2(float lo, float hi) {
   uint64_t p;
   asm("mov.b64 %0, {%1, %2};" : "=l"(p) : "f"(lo), "f"(hi));
@@ -290,6 +309,32 @@ DEVI float2 unpack2(uint64_t p) {
   float lo, hi;
   asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(p));
   return make_float2(lo, hi);
+}
+
+
+// ------------------------------------------------ TMEM stores / A operand ----
+// 32 lanes x 32 consecutive columns from registers (thread t -> lane
+// (warp%4)*32 + t); completion via tmem_st_wait().
+DEVI void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%"
+      "19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+DEVI void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// D[tmem] (+)= A[tmem] . B[smem]^T  (kind::i8, A in tensor memory: lane = row
+// of A, 4 consecutive int8 K-elements per 32-bit column)
+DEVI void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
 }
 
 }  // namespace comet

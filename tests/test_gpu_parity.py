@@ -37,7 +37,10 @@ def gpu_path(p, group, want_acc=False, planes_only=False):
         if want_acc:
             out["Acc"] = comet.comet_w4ax_gemm_acc_i32(Xq8, Xq4, Sx, bits, Wq, Sw, group)
     torch.cuda.synchronize()
-    return {k: v.cpu().numpy() for k, v in out.items()}
+    res = {k: v.cpu().numpy() for k, v in out.items()}
+    N, K = p["W"].shape
+    res["Wq"] = comet.wq_tiled_to_rowmajor(res["Wq"], N, K)  # layout only
+    return res
 
 
 def oracle_path(p, group, rows=None, want_acc=False):
