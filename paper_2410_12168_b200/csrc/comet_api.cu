@@ -471,6 +471,9 @@ int comet_debug_cta_times(int enable, unsigned long long* host, int n) {
   }
   return 0;
 }
+int comet_debug_role_cycles(unsigned long long* host12) {
+  return cudaMemcpyFromSymbol(host12, g_role_cycles, sizeof(unsigned long long) * 12) == cudaSuccess ? 0 : -1;
+}
 int64_t comet_launch_count(void) { return g_launches.load(); }
 
 }  // extern "C"

@@ -94,6 +94,33 @@ DEVI unsigned long long global_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+DEVI unsigned long long clk64() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+  return t;
+}
+// debug: per-role wait cycles of CTA 0: [role][0..2] = wait A, wait B, total
+__device__ unsigned long long g_role_cycles[4][3];
+struct RoleTimer {
+  bool on;
+  unsigned long long t0, w[2];
+  DEVI RoleTimer(bool enabled) : on(enabled), t0(enabled ? clk64() : 0) { w[0] = w[1] = 0; }
+  DEVI void wait(uint64_t* bar, uint32_t parity, int k) {
+    if (!on) {
+      mbar_wait(bar, parity);
+      return;
+    }
+    const unsigned long long a = clk64();
+    mbar_wait(bar, parity);
+    w[k] += clk64() - a;
+  }
+  DEVI void flush(int role) {
+    if (!on) return;
+    g_role_cycles[role][0] = w[0];
+    g_role_cycles[role][1] = w[1];
+    g_role_cycles[role][2] = clk64() - t0;
+  }
+};
 DEVI uint32_t smid() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
@@ -169,6 +196,7 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------- a3: producer ----
     const uint64_t pol_w = l2_policy_evict_first();
+    RoleTimer rt(g_cta_times_on && blockIdx.x == 0 && lane == 0);
     int t = u0 / nb, b = u0 - t * nb;
     int n0, m0;
     tile_coords(t, n0, m0);
@@ -177,7 +205,7 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
       const uint32_t code = map.code[b];
       const bool is8 = (code >> 15) != 0;
       const int rank = code & 0x7FFF;
-      mbar_wait(&empty[s], ((i / C::kStages) & 1) ^ 1);
+      rt.wait(&empty[s], ((i / C::kStages) & 1) ^ 1, 0);
       uint8_t* st = smem + s * C::kStageBytes;
       if (elect_one()) {
         mbar_arrive_expect_tx(&full[s], C::kWPBytes + (is8 ? C::kBBytes : C::kXPBytes));
@@ -189,7 +217,7 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
       }
       if (!kAccOut) {
         const int a = i % C::kScaleSlots;
-        mbar_wait(&sempty[a], ((i / C::kScaleSlots) & 1) ^ 1);
+        rt.wait(&sempty[a], ((i / C::kScaleSlots) & 1) ^ 1, 1);
         if (elect_one()) {
           const bool seg_end = (b == nb - 1) || (i == nu - 1);
           const int nsx = max(0, min(BN, (int)args.ldsx - m0));  // multiple of 4
@@ -207,14 +235,16 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
         if (t < sched.tiles) tile_coords(t, n0, m0);
       }
     }
+    rt.flush(0);
   } else if (warp == 1) {
     // ------------------------------------------------------ a5: MMA ----
     constexpr uint32_t idesc = idesc_i8(128, BN);
+    RoleTimer rt(g_cta_times_on && blockIdx.x == 0 && lane == 0);
     for (int i = 0; i < nu; ++i) {
       const int s = i % C::kStages;
       const int acc = i % C::kAcc;
-      mbar_wait(&tempty[acc], ((i / C::kAcc) & 1) ^ 1);
-      mbar_wait(&expd[s], (i / C::kStages) & 1);
+      rt.wait(&tempty[acc], ((i / C::kAcc) & 1) ^ 1, 0);
+      rt.wait(&expd[s], (i / C::kStages) & 1, 1);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t b0 = sbase + s * C::kStageBytes + C::kWPBytes;
@@ -229,6 +259,7 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
       }
       __syncwarp();
     }
+    rt.flush(1);
   } else if (warp >= 4 && warp < C::kEpiWarp0) {
     // ------------------------------------------ a4: expansion warps ----
     const int q = warp & 3;
@@ -236,13 +267,14 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
     const int grp = (warp - 4) >> 2;
     const int tid = threadIdx.x - 128 - 128 * grp;
     int b = (u0 + grp) % nb;
+    RoleTimer rt(g_cta_times_on && blockIdx.x == 0 && warp == 4 && lane == 0);
     for (int i = grp; i < nu; i += C::kExpGroups) {
       const int s = i % C::kStages;
       const bool is8 = (map.code[b] >> 15) != 0;
       b += C::kExpGroups;
       if (b >= nb) b -= nb;
       const uint32_t st = sbase + s * C::kStageBytes;
-      mbar_wait(&full[s], (i / C::kStages) & 1);
+      rt.wait(&full[s], (i / C::kStages) & 1, 0);
       // own weight row: 4 x 16 B, 64B-swizzled (chunk c at c ^ ((row >> 1) & 3))
       uint32_t e[32];
 #pragma unroll
@@ -257,7 +289,7 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
         }
       }
       const int as = i % C::kASlots;
-      mbar_wait(&aempty[as], ((i / C::kASlots) & 1) ^ 1);  // MMA of unit i - kASlots done
+      rt.wait(&aempty[as], ((i / C::kASlots) & 1) ^ 1, 1);  // MMA of unit i - kASlots done
       tc_fence_after();
       tmem_st_32x32b_x32(tmem_base + ((uint32_t)(32 * q) << 16) + C::kAOff + 32 * as, e);
       if (!is8) {
@@ -282,6 +314,7 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&expd[s]);
     }
+    rt.flush(2);
   } else if (warp >= C::kEpiWarp0) {
     // ----------------------------------------- a6-a8: epilogue warps ----
     const int q = warp & 3;
@@ -294,6 +327,7 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
     for (int j = 0; j < C::kCW; ++j) y[j] = 0.f;
     int t = u0 / nb, b = u0 - t * nb;
     int seg_first = b;  // first block of the current segment
+    RoleTimer rt(g_cta_times_on && blockIdx.x == 0 && warp == C::kEpiWarp0 && lane == 0);
     for (int i = 0; i < nu; ++i) {
       const int acc = i % C::kAcc;
       const int a = i % C::kScaleSlots;
@@ -304,11 +338,11 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
       const int n = n0 + row;
       float swv = 0.f;
       if (!kAccOut) {
-        mbar_wait(&sfull[a], (i / C::kScaleSlots) & 1);
+        rt.wait(&sfull[a], (i / C::kScaleSlots) & 1, 0);
         swv = kGroupK ? 1.f : lds_f32(slot + BN * 4 + row * 4);
         swv *= is8 ? 0.0625f : 0.00390625f;  // fold 16^-e
       }
-      mbar_wait(&tfull[acc], (i / C::kAcc) & 1);
+      rt.wait(&tfull[acc], (i / C::kAcc) & 1, 1);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < C::kCW; c += C::kChunk) {
@@ -416,6 +450,7 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
       }
       if (seg_end) seg_first = b;
     }
+    rt.flush(3);
   }
 
   tc_fence_before();

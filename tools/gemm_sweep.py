@@ -65,3 +65,21 @@ def slow_ctas(M, N, K, n8):
         d = (a[:, 1] - a[:, 0]) / 1e3
         o = np.argsort(-d)
         print(f"M={M} N={N}: slowest", [(int(i), round(float(d[i]), 1), int(a[i, 2])) for i in o[:5]], "median", round(float(np.median(d)), 1))
+
+
+def roles(M, N, K, n8):
+    import ctypes
+    L = comet.lib()
+    L.comet_debug_cta_times.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
+    L.comet_debug_role_cycles.argtypes = [ctypes.c_void_p]
+    L.comet_debug_cta_times(1, None, 0)
+    run(M, N, K, n8, "K", reps=1)
+    L.comet_debug_cta_times(0, None, 0)
+    buf = (ctypes.c_ulonglong * 12)()
+    L.comet_debug_role_cycles(buf)
+    a = np.array(buf[:], dtype=np.int64).reshape(4, 3)
+    names = [("producer", "wait empty", "wait sempty"), ("mma", "wait tempty", "wait expd"),
+             ("expand g0", "wait full", "wait aempty"), ("epilogue", "wait sfull", "wait tfull")]
+    print(f"M={M} N={N} K={K} CTA0 roles (cycles):")
+    for (n, w0, w1), row in zip(names, a):
+        print(f"  {n:10s} total {row[2]:8d}  {w0} {row[0]:8d} ({row[0]/max(row[2],1):.0%})  {w1} {row[1]:8d} ({row[1]/max(row[2],1):.0%})")
