@@ -73,7 +73,7 @@ def load_traffic(config_name):
 
 # ------------------------------------------------------------ clocks ----
 class ClockSampler:
-    def __init__(self, dev_index=0, period=0.05):
+    def __init__(self, dev_index=0, period=0.005):
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self.period, self._stop = period, threading.Event()
         try:
@@ -89,7 +89,8 @@ class ClockSampler:
                0x80: "hw_power_brake_slowdown", 0x4: "sw_power_cap", 0x1: "gpu_idle"}
 
     def _run(self):
-        while not self._stop.is_set():
+        while True:
+            stop = self._stop.is_set()
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
@@ -98,6 +99,8 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
+            if stop:
+                break
             time.sleep(self.period)
 
     def __enter__(self):
@@ -253,14 +256,19 @@ def run_comet(args, cfg, config_name):
         Yh = torch.empty((M, per), dtype=torch.float16).pin_memory()
         scratch = comet.new_workspace(comet.comet_w4ax_linear_scratch_bytes(M, per, K, bits), dev)
         layers.append(dict(N=N, K=K, grp=grp, per=per, W=W, perm=perm, bits=bits, Wq=Wq, Sw=Sw, X=X, planes=planes, Y=Y,
-                           ws=ws, Yall=Yall, Xh=Xh, Yh=Yh, scratch=scratch, ev=[]))
+                           ws=ws, Yall=Yall, Xh=Xh, Yh=Yh, scratch=scratch, ev=[], qev=[]))
         del p
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     def step(timed_kernels=False):
         for L in layers:
+            if timed_kernels:
+                qa, qb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                qa.record(stream)
             Xq8, Xq4, Sx = comet.comet_quantize_act(L["X"], L["bits"], L["perm"], out=L["planes"])
             if timed_kernels:
+                qb.record(stream)
+                L["qev"].append((qa, qb))
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
             comet.comet_w4ax_gemm(Xq8, Xq4, Sx, L["bits"], L["Wq"], L["Sw"], L["grp"], out=L["Y"], workspace=L["ws"])
@@ -295,6 +303,7 @@ def run_comet(args, cfg, config_name):
     launches = comet.launch_count() - n_launch0
     t_dev = sum(a.elapsed_time(b) for a, b in step_ms) / args.steps  # ms per step
     gemm_ms = [sum(a.elapsed_time(b) for a, b in L["ev"]) / len(L["ev"]) for L in layers]
+    quant_ms = [sum(a.elapsed_time(b) for a, b in L["qev"]) / len(L["qev"]) for L in layers]
     L0 = layers[0]
 
     # ---- end-to-end through the C ABI with host buffers ----
@@ -356,6 +365,11 @@ def run_comet(args, cfg, config_name):
                       "l2": "flushed (256 MiB write) before every timed step, outside the events"},
            "tokens_per_s": M / (t_dev * 1e-3),
            "gemm_us": [g * 1e3 for g in gemm_ms],
+           "quantize_us": [q * 1e3 for q in quant_ms],
+           "quantize_hbm": {"achieved_gbs": [ (2 * M * L["K"] + M * (128 * L["bits"].n8 + 64 * L["bits"].n4)
+                                               + 4 * M * (L["K"] // 128)) / (q * 1e-3) / 1e9
+                                              for L, q in zip(layers, quant_ms)],
+                            "peak_gbs": peaks["hbm_gbs"]},
            "pack_weight_ms": t_pack,
            "e2e": {"value": e2e_tops, "unit": "TOPS", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                    "ms_per_step": e2e_t, "api": "comet_w4ax_linear (host pinned X in, host Y out)"},
