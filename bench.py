@@ -132,14 +132,6 @@ def dist_setup(ngpus):
     return 0, 1, 0
 
 
-def shard_rows(N, world, rank, align=128):
-    """Column-parallel shard [n0, n1) of the N output channels (multiples of 128, equal padded width)."""
-    per = -(-N // world)
-    per = -(-per // align) * align
-    n0 = min(rank * per, N)
-    return n0, min(n0 + per, N), per
-
-
 # ---------------------------------------------------------- reference ----
 def run_reference(args, cfg):
     """--impl reference: the CPU oracle as it stands on the host cores."""
@@ -222,7 +214,7 @@ def cpu_baseline(cfg, args, seconds_target=10.0):
 def run_comet(args, cfg, config_name):
     import torch
     import torch.distributed as dist
-    from paper_2410_12168_b200 import comet, synth
+    from paper_2410_12168_b200 import comet, synth, tp
 
     rank, world, local = dist_setup(args.gpus)
     dev = torch.device("cuda", local)
@@ -234,10 +226,8 @@ def run_comet(args, cfg, config_name):
     t_pack = 0.0
     for li, ((N, K), n8) in enumerate(zip(cfg["layers"], cfg["n8"])):
         p = synth.make_problem(M, N, K, n8=n8, seed=100 + li)
-        n0, n1, per = shard_rows(N, world, rank)
-        Wl = np.zeros((per, K), np.float16)
-        Wl[: n1 - n0] = p["W"][n0:n1]
-        W = torch.from_numpy(Wl).to(dev)
+        n0, n1, per = tp.shard_rows(N, world, rank)
+        W = torch.from_numpy(tp.shard_weight(p["W"], world, rank)).to(dev)
         perm = torch.from_numpy(p["perm"]).to(dev)
         bits = comet.BlockBits(p["bits"])
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -276,7 +266,7 @@ def run_comet(args, cfg, config_name):
                 b.record(stream)
                 L["ev"].append((a, b))
             if world > 1:
-                dist.all_gather_into_tensor(L["Yall"], L["Y"])
+                tp.all_gather_y(L["Y"], out=L["Yall"])
 
     def barrier():
         if world > 1:

@@ -1,0 +1,87 @@
+"""N>1 path on CPU: world_size-2 gloo run of the N-sharded W4Ax layer
+(-m "not gpu").  The per-rank GEMM is the oracle here (no GPU); the sharding,
+the all_gather and the reassembly are the product code (tp.py) that bench.py
+runs over NCCL on GPUs.  The gathered Y must equal the single-process Y
+bit for bit (each output channel depends only on its own weight row)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2410_12168_b200 import synth, tp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, M, N, K, group, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = synth.make_problem(M, N, K, n8=1, seed=31)
+        Wl = tp.shard_weight(p["W"], world, rank)
+        g = K if group == "K" else 128
+        Xq8, Xq4, Sx = oracle.quantize_act(p["X"], p["bits"], p["perm"])
+        Wq, Sw = oracle.pack_weight(Wl, g, p["perm"])
+        y = oracle.w4ax_gemm(Xq8, Xq4, Sx, p["bits"], Wq, Sw, group=g)["y"]
+        # gloo has no fp16/int16 transport: carry the fp16 values in fp32 (exact)
+        y_all = tp.all_gather_y(torch.from_numpy(y.astype(np.float32)))
+        full = tp.gathered_to_full(y_all, N).numpy().astype(np.float16)
+        # every rank's activation planes are identical (replicated X)
+        digest = torch.tensor([int(Xq4.astype(np.int64).sum()), int(Xq8.astype(np.int64).sum())])
+        allx = [torch.zeros_like(digest) for _ in range(world)]
+        dist.all_gather(allx, digest)
+        q.put((rank, full, [t.tolist() for t in allx]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("N,group", [(640, 128), (512, "K"), (1152, 128)])
+def test_n_sharded_allgather_equals_single_process(N, group):
+    M, K, world = 12, 512, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, M, N, K, group, q)) for r in range(world)]
+    for p_ in procs:
+        p_.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    p = synth.make_problem(M, N, K, n8=1, seed=31)
+    g = K if group == "K" else 128
+    Xq8, Xq4, Sx = oracle.quantize_act(p["X"], p["bits"], p["perm"])
+    Wq, Sw = oracle.pack_weight(p["W"], g, p["perm"])
+    ref = oracle.w4ax_gemm(Xq8, Xq4, Sx, p["bits"], Wq, Sw, group=g)["y"]
+    for rank, full, digests in res:
+        assert np.array_equal(full.view(np.uint16), ref.view(np.uint16)), rank
+        assert all(d == digests[0] for d in digests)
+
+
+def test_shard_rows_cover_and_align():
+    for N in (4096, 11008, 57344, 8192, 10240, 640):
+        for world in (1, 2, 4, 8):
+            seen = []
+            for r in range(world):
+                n0, n1, per = tp.shard_rows(N, world, r)
+                assert per % 128 == 0 and n1 - n0 <= per
+                seen.extend(range(n0, n1))
+            assert seen == list(range(N))
+
+
+def test_gathered_to_full_layout():
+    y_all = torch.arange(2 * 3 * 4).reshape(2, 3, 4)
+    full = tp.gathered_to_full(y_all, 7)
+    assert full.tolist() == [[0, 1, 2, 3, 12, 13, 14], [4, 5, 6, 7, 16, 17, 18], [8, 9, 10, 11, 20, 21, 22]]
