@@ -50,6 +50,16 @@ DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// non-blocking probe (no suspend), acquire at cluster scope
+DEVI bool mbar_test_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 
 // ----------------------------------------------------------------- TMA ----
 DEVI void tma_prefetch_desc(const CUtensorMap* m) {
@@ -335,6 +345,38 @@ DEVI void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t 
       " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
+}
+
+
+// 32 lanes x 16 columns from registers
+DEVI void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+// 32 lanes x 16 columns, every column set to v
+DEVI void tmem_fill_32x32b_x16(uint32_t taddr, uint32_t v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(v)
+      : "memory");
+}
+
+// Magic-biased accumulators: an INT32 accumulator that starts at the bit
+// pattern 0x4B400000 (= 1.5*2^23 as fp32) holds, after the MMA adds an exact
+// integer a with |a| < 2^22, the fp32 value 1.5*2^23 + a exactly.  Subtracting
+// 1.5*2^23 (FADD2, exact by Sterbenz) yields float(a): two INT32 -> fp32
+// conversions per FMA-pipe instruction instead of one I2F each on the
+// half-rate ALU pipe.  Bit-identical to cvt.rn.f32.s32.
+constexpr uint32_t kAccMagic = 0x4B400000u;
+DEVI void magic_fma2(uint64_t& y, uint32_t a0, uint32_t a1, uint64_t s) {
+  asm("{\n .reg .b64 p;\n mov.b64 p, {%1, %2};\n add.rn.f32x2 p, p, %4;\n fma.rn.f32x2 %0, p, %3, %0;\n}\n"
+      : "+l"(y)
+      : "r"(a0), "r"(a1), "l"(s), "l"(0xCB400000CB400000ull));
 }
 
 }  // namespace comet

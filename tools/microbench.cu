@@ -77,6 +77,32 @@ __global__ void __launch_bounds__(512) tmem_ld_kernel(float* out, long long* cyc
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+template <int NWARPS>
+__global__ void __launch_bounds__(512) tmem_st_kernel(float* out, long long* cyc) {
+  __shared__ uint32_t holder;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc<512>(&holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t base = holder;
+  long long t0 = clock64();
+  if (warp < NWARPS) {
+    const uint32_t q = warp & 3;
+    for (int i = 0; i < ITERS / 8; ++i) {
+      tmem_fill_32x32b_x16(base + (q << 16) * 32 + ((i * 16 + (warp >> 2) * 128) & 511), 0x4B400000u + i);
+      tmem_fill_32x32b_x16(base + (q << 16) * 32 + ((i * 16 + 16 + (warp >> 2) * 128) & 511), 0x4B400000u + i);
+    }
+    tmem_st_wait();
+  }
+  long long t1 = clock64();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(base);
+  out[blockIdx.x * blockDim.x + threadIdx.x] = 0.f;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 template <typename F>
 void report(const char* name, F launch, double work_per_cta) {
   float* out;
@@ -111,6 +137,9 @@ int main() {
   const double ld_bytes = (ITERS / 8) * 32.0 * 32 * 4;  // per warp
   report("tcgen05.ld B/clk, 4 warps", [](float* o, long long* c) { tmem_ld_kernel<4><<<148, 512>>>(o, c); }, 4 * ld_bytes);
   report("tcgen05.ld B/clk, 8 warps", [](float* o, long long* c) { tmem_ld_kernel<8><<<148, 512>>>(o, c); }, 8 * ld_bytes);
+  const double st_bytes = (ITERS / 8) * 2 * 16.0 * 32 * 4;  // per warp
+  report("tcgen05.st B/clk, 4 warps", [](float* o, long long* c) { tmem_st_kernel<4><<<148, 512>>>(o, c); }, 4 * st_bytes);
+  report("tcgen05.st B/clk, 16 warps", [](float* o, long long* c) { tmem_st_kernel<16><<<148, 512>>>(o, c); }, 16 * st_bytes);
   report("tcgen05.ld B/clk, 16 warps", [](float* o, long long* c) { tmem_ld_kernel<16><<<148, 512>>>(o, c); }, 16 * ld_bytes);
   return 0;
 }
