@@ -88,6 +88,22 @@ bool make_map_u8(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows,
   return r == CUDA_SUCCESS;
 }
 
+// 2-D fp32 tensor [rows x cols] (row stride ld elements), box [box_rows x box_cols],
+// out-of-bounds elements zero-filled
+bool make_map_f32(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t ld, uint32_t box_cols,
+                  uint32_t box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // ---- block map ------------------------------------------------------------
 bool build_block_map(const uint8_t* bits, int nb, BlockMap* map, int* n8, int* n4) {
   int r8 = 0, r4 = 0;
@@ -136,6 +152,7 @@ Plan make_plan(int M, int N, int K, int num_sms) {
   p.clusters = (int)(units < num_sms ? units : num_sms);  // CTAs
   p.ws_bytes = kCounterBytes + (int64_t)p.clusters * 2 * 128 * p.bn * 4;
   if (tiles > kCounterBytes / 4) p.ws_bytes = -1;  // more tiles than tile counters
+  if (units * p.clusters >= (int64_t)1 << 32) p.ws_bytes = -1;  // kernel's 32-bit stream-K split arithmetic
   return p;
 }
 
@@ -158,8 +175,12 @@ comet_status launch_gemm_2sm(const CUtensorMap& tmW, const CUtensorMap& tmX4, co
   return check_launch();
 }
 
+struct DecMaps {
+  CUtensorMap sx, sw;  // Sx [nb x ldsx] box [kUB x BN]; Sw [nb x N] box [kUB x 128] (group 128)
+};
+
 template <int BN, bool kGroupK, bool kAcc>
-comet_status launch_decode(const CUtensorMap& tmW, const CUtensorMap& tmX4, const CUtensorMap& tmX8,
+comet_status launch_decode(const DecMaps& dm, const CUtensorMap& tmX4, const CUtensorMap& tmX8,
                            const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
   using C = DecCfg<BN>;
   auto kern = w4ax_gemm_decode_kernel<BN, kGroupK, kAcc>;
@@ -170,20 +191,36 @@ comet_status launch_decode(const CUtensorMap& tmW, const CUtensorMap& tmX4, cons
   DecSched sched;
   sched.n_tiles = p.n_tiles;
   sched.tiles = p.n_tiles * p.m_tiles;
-  sched.units = sched.tiles * args.nb;
+  sched.units = sched.tiles * args.nb;  // K-blocks: the split granularity
   sched.ctas = p.clusters;
-  kern<<<sched.ctas, C::kThreads, C::kSmemBytes, st>>>(tmW, tmX4, tmX8, map, args, sched);
+  kern<<<sched.ctas, C::kThreads, C::kSmemBytes, st>>>(dm.sx, tmX4, tmX8, dm.sw, map, args, sched);
   return check_launch();
 }
 
+template <int BN, bool kGroupK, bool kAcc>
+comet_status launch_decode_maps(const CUtensorMap& tmX4, const CUtensorMap& tmX8, const BlockMap& map,
+                                const GemmArgs& args, const Plan& p, cudaStream_t st) {
+  constexpr int kUB = DecCfg<BN>::kUB;
+  DecMaps dm;
+  if (!make_map_f32(&dm.sx, args.Sx, (uint64_t)args.ldsx, (uint64_t)args.nb, (uint64_t)args.ldsx, BN, kUB))
+    return COMET_ERR_CUDA;
+  if (!kGroupK && !kAcc) {
+    if (!make_map_f32(&dm.sw, args.Sw, (uint64_t)args.N, (uint64_t)args.nb, (uint64_t)args.N, 128, kUB))
+      return COMET_ERR_CUDA;
+  } else {
+    dm.sw = dm.sx;  // never dereferenced
+  }
+  return launch_decode<BN, kGroupK, kAcc>(dm, tmX4, tmX8, map, args, p, st);
+}
+
 template <bool kGroupK, bool kAcc>
-comet_status launch_decode_bn(const CUtensorMap& tmW, const CUtensorMap& tmX4, const CUtensorMap& tmX8,
-                              const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
+comet_status launch_decode_bn(const CUtensorMap& tmX4, const CUtensorMap& tmX8, const BlockMap& map,
+                              const GemmArgs& args, const Plan& p, cudaStream_t st) {
   switch (p.bn) {
-    case 16: return launch_decode<16, kGroupK, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
-    case 32: return launch_decode<32, kGroupK, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
-    case 64: return launch_decode<64, kGroupK, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
-    default: return launch_decode<128, kGroupK, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
+    case 16: return launch_decode_maps<16, kGroupK, kAcc>(tmX4, tmX8, map, args, p, st);
+    case 32: return launch_decode_maps<32, kGroupK, kAcc>(tmX4, tmX8, map, args, p, st);
+    case 64: return launch_decode_maps<64, kGroupK, kAcc>(tmX4, tmX8, map, args, p, st);
+    default: return launch_decode_maps<128, kGroupK, kAcc>(tmX4, tmX8, map, args, p, st);
   }
 }
 
@@ -195,8 +232,8 @@ comet_status launch_gemm(const CUtensorMap& tmW, const CUtensorMap& tmX4, const 
     if (group_k) return launch_gemm_2sm<true, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
     return launch_gemm_2sm<false, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
   }
-  if (group_k) return launch_decode_bn<true, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
-  return launch_decode_bn<false, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
+  if (group_k) return launch_decode_bn<true, kAcc>(tmX4, tmX8, map, args, p, st);
+  return launch_decode_bn<false, kAcc>(tmX4, tmX8, map, args, p, st);
 }
 
 comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx, const uint8_t* bits,
@@ -471,8 +508,11 @@ int comet_debug_cta_times(int enable, unsigned long long* host, int n) {
   }
   return 0;
 }
-int comet_debug_role_cycles(unsigned long long* host12) {
-  return cudaMemcpyFromSymbol(host12, g_role_cycles, sizeof(unsigned long long) * 12) == cudaSuccess ? 0 : -1;
+int comet_debug_role_cycles(unsigned long long* host16) {
+  return cudaMemcpyFromSymbol(host16, g_role_cycles, sizeof(unsigned long long) * 16) == cudaSuccess ? 0 : -1;
+}
+int comet_debug_trace(unsigned long long* host768) {
+  return cudaMemcpyFromSymbol(host768, g_trace, sizeof(unsigned long long) * 768) == cudaSuccess ? 0 : -1;
 }
 int64_t comet_launch_count(void) { return g_launches.load(); }
 

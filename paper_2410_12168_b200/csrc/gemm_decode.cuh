@@ -10,21 +10,22 @@
 // arriving contributor, summing the partials in CTA order (deterministic),
 // after the single inter-CTA sync before write-back.
 //
-// Per unit (one 128-channel block of one tile):
-//   a3  warp 0: 1-D bulk copy of the packed weight slab [128 rows x 64 B],
-//       contiguous in the tiled weight layout with the 64B swizzle baked in
-//       (evict-first: read once), TMA of the token slab (INT8 blocks
-//       straight into the SW128 MMA operand, INT4 blocks packed), plus 1-D
-//       bulk copies of the block's scales into a scale ring;
+// Per unit (up to kUB consecutive 128-channel blocks of one tile):
+//   a3  warp 0: one 1-D bulk copy of the unit's packed weight slabs
+//       [kUB x 128 rows x 64 B], contiguous in the tiled weight layout with the
+//       64B swizzle baked in (evict-first: read once); a TMA of each block's
+//       token slab (INT8 blocks straight into the SW128 MMA operand, INT4
+//       blocks packed) and a 2-D TMA box of the unit's scales into a scale
+//       ring -- the token/scale loads are issued by warp 2 so the weight
+//       stream's issue path stays short;
 //   a4  warps 4-7 / 8-11 (two groups taking alternate units; thread = weight
-//       row): 4 x LDS.128 of the row, INT4->INT8
-//       zero-extension in registers, tcgen05.st of the 32 expanded
-//       columns into this stage's TMEM A slot; INT4 token blocks are expanded
-//       into smem;
-//   a5  warp 1: 4 x tcgen05.mma.kind::i8 (A from TMEM, M=128, N=BN, K=32)
-//       into a fresh INT32 accumulator (kAcc-deep TMEM ring);
+//       row): per block 4 x LDS.128 of the row, INT4->INT8 zero-extension in
+//       registers, tcgen05.st of the 32 expanded columns into the
+//       unit's TMEM A slot; INT4 token blocks are expanded into smem;
+//   a5  warp 1: per block 4 x tcgen05.mma.kind::i8 (A from TMEM, M=128, N=BN,
+//       K=32) into a fresh INT32 accumulator (kAcc-deep TMEM ring of units);
 //   a6  epilogue warps (thread = weight row, columns = tokens):
-//       y[m] += (sw[n] sx[m,b] 16^-e_b) * acc[m];
+//       y[m] += (sw[n] sx[m,b] 16^-e_b) * acc_b[m] for each block b;
 //   a7/a8 segment end: fp16 store, or fp32 partial + last-arriver fixup.
 #pragma once
 #include <cuda_fp16.h>
@@ -34,43 +35,102 @@
 #include "quantize.cuh"
 #include "sm100.cuh"
 
+#ifndef COMET_DEC_EXP
+#define COMET_DEC_EXP 0  // timing experiments only: 1 = skip Sx loads, 2 = also skip X loads
+#endif
+
 namespace comet {
 
 template <int BN>
 struct DecCfg {
-  // smem stages set the HBM bytes in flight per SM (a stage is recycled only
-  // after HBM latency + expansion + MMA); TMEM A slots only span expansion ->
-  // MMA completion, so they are a separate, shorter ring
-  static constexpr int kStages = BN <= 16 ? 16 : (BN == 32 ? 14 : (BN == 64 ? 10 : 6));
-  static constexpr int kASlots = 4;
-  static constexpr int kAcc = BN <= 32 ? 8 : (BN == 64 ? 4 : 2);
-  static constexpr int kWPBytes = 128 * 64;  // packed weights, 64B swizzle
-  static constexpr int kBBytes = BN * 128;   // tokens int8, SW128 K-major
-  static constexpr int kXPBytes = BN * 64;   // packed INT4 tokens
-  static constexpr int kStageBytes = kWPBytes + kBBytes + kXPBytes;  // multiple of 1024 (BN >= 16)
-  static constexpr int kSlotBytes = BN * 4 + 128 * 4;                // sx[BN] + sw[128]
-  static constexpr int kScaleSlots = 16;
-  static constexpr int kAOff = kAcc * BN;                            // TMEM column of the A slots
+  // a unit is up to kUB consecutive K-blocks of one tile: one contiguous
+  // kUB x 8 KB weight copy, one set of barrier hand-offs and one accumulator
+  // slot of kUB x BN columns per unit (the fixed per-unit cost of every role
+  // is paid once per kUB blocks)
+  static constexpr int kUB = BN <= 32 ? 4 : (BN == 64 ? 2 : 1);
+  static constexpr int kWPBytes = 128 * 64;  // packed weights of one block, 64B swizzle
+  static constexpr int kBBytes = BN * 128;   // tokens int8 of one block, SW128 K-major
+  static constexpr int kXPBytes = BN * 64;   // packed INT4 tokens of one block
+  // two smem rings: weights [kUB x kWPBytes], released by the expansion warps
+  // as soon as they have read them (the MMA never touches packed weights), and
+  // tokens [B: kUB x kBBytes][XP: kUB x kXPBytes], released by the MMA commit
+  static constexpr int kWStageBytes = kUB * kWPBytes;
+  static constexpr int kXStageBytes = kUB * (kBBytes + kXPBytes);
+  static constexpr int kXPOff = kUB * kBBytes;  // within a token stage
+  // weight stages set the HBM bytes in flight per SM
+  static constexpr int kWStages = BN == 16 ? 5 : (BN == 32 ? 4 : (BN == 64 ? 7 : 10));
+  static constexpr int kXStages = BN == 128 ? 4 : 3;
+  static constexpr int kXBase = kWStages * kWStageBytes;
+  // scale slot = [sx: kUB x BN][sw: kUB x 128] fp32
+  static constexpr int kSxBytes = kUB * BN * 4;
+  static constexpr int kSlotBytes = kSxBytes + kUB * 128 * 4;
+  static constexpr int kScaleSlots = BN <= 32 ? 6 : 8;
+  static constexpr int kScaleBase = kXBase + kXStages * kXStageBytes;
+  static constexpr int kBarBase = kScaleBase + kScaleSlots * kSlotBytes;
+  // TMEM: kAcc accumulator slots of kUB x BN columns, then kASlots weight
+  // (A operand) slots of kUB x 32 columns
+  static constexpr int kASlots = BN == 16 ? 3 : (kUB == 1 ? 4 : 2);
+  static constexpr int kAccCols = kUB * BN;
+  static constexpr int kAccMax = (512 - kASlots * 32 * kUB) / kAccCols;
+  static constexpr int kAcc = kAccMax > 8 ? 8 : kAccMax;
+  static constexpr int kAOff = kAcc * kAccCols;  // TMEM column of the A slots
   static constexpr int kTmemCols = 512;
-  static constexpr int kEpiWarps = BN >= 128 ? 8 : 4;
-  static constexpr int kCW = BN / (kEpiWarps / 4);                   // columns per epilogue warp
+  // two column halves x 4 lane quarters
+  static constexpr int kEpiWarps = 8;
+  static constexpr int kCW = BN / (kEpiWarps / 4);  // columns per epilogue warp
   static constexpr int kChunk = kCW >= 16 ? 16 : kCW;
+  // blocks whose accumulators are loaded before one tcgen05.wait::ld
+  static constexpr int kLdG0 = 32 / kCW > 0 ? 32 / kCW : 1;
+  static constexpr int kLdG = kLdG0 < kUB ? kLdG0 : kUB;
   // expansion groups of 4 warps (one per TMEM lane quarter) take alternate
   // units, so two units' LDS -> zero-extend -> tcgen05.st chains overlap
   static constexpr int kExpGroups = BN >= 128 ? 1 : 2;
   static constexpr int kEpiWarp0 = 4 + 4 * kExpGroups;
   static constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
-  static constexpr int kSmemNeed = kStages * kStageBytes + kScaleSlots * kSlotBytes + 512 + 1024;
+  static constexpr int kSmemNeed = kBarBase + 1024 + 1024;
   // > half of the SM's 228 KB: exactly one CTA per SM (stream-K divides the
   // work by CTA, and each CTA owns all 512 TMEM columns)
   static constexpr int kSmemBytes = kSmemNeed > 120 * 1024 ? kSmemNeed : 120 * 1024;
-  static_assert(kAOff + 32 * kASlots <= kTmemCols, "TMEM budget");
+  static_assert(kAcc >= 2, "TMEM budget");
+  static_assert(kAOff + 32 * kUB * kASlots <= kTmemCols, "TMEM budget");
   static_assert(kSmemNeed <= 227 * 1024, "smem budget");
+  static_assert(kXBase % 1024 == 0 && kXStageBytes % 1024 == 0 && kBBytes % 1024 == 0, "SW128 alignment");
 };
 
 struct DecSched {
-  int n_tiles, tiles, units, ctas;  // units = tiles * nb
-  DEVI int u_begin(int c) const { return (int)(((int64_t)units * c) / ctas); }
+  int n_tiles, tiles, units, ctas;  // units = tiles * nb K-blocks (the stream-K split granularity)
+  // 32-bit: the host guarantees units * ctas < 2^32 (tiles <= 16384, nb <= 512)
+  DEVI int u_begin(int c) const { return (int)(((uint32_t)units * (uint32_t)c) / (uint32_t)ctas); }
+};
+
+// walks a CTA's block range [u, u1) in units of up to KUB blocks that never
+// cross a tile boundary; every role replays the same sequence
+template <int KUB>
+struct UnitIt {
+  int u, u1, t, b, len;  // global block index, range end, tile, block in tile, blocks in unit
+  int tn, tm, n_tiles;   // tile t = tm * n_tiles + tn (channel tile tn fastest), kept without division
+  DEVI UnitIt(int u0_, int u1_, int nb, int n_tiles_) : u(u0_), u1(u1_), n_tiles(n_tiles_) {
+    t = u / nb;
+    b = u - t * nb;
+    tm = t / n_tiles;
+    tn = t - tm * n_tiles;
+    set_len(nb);
+  }
+  DEVI void set_len(int nb) { len = min(min(KUB, nb - b), u1 - u); }
+  DEVI bool valid() const { return u < u1; }
+  DEVI void next(int nb) {
+    u += len;
+    b += len;
+    if (b == nb) {
+      b = 0;
+      ++t;
+      if (++tn == n_tiles) {
+        tn = 0;
+        ++tm;
+      }
+    }
+    set_len(nb);
+  }
 };
 
 template <int N>
@@ -99,12 +159,17 @@ DEVI unsigned long long clk64() {
   asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
   return t;
 }
-// debug: per-role wait cycles of CTA 0: [role][0..2] = wait A, wait B, total
-__device__ unsigned long long g_role_cycles[4][3];
+// debug: per-role cycles of CTA g_cta_times_on - 1:
+// [role][0..3] = wait A, wait B, total, stream-K fixup (epilogue)
+__device__ unsigned long long g_role_cycles[4][4];
 struct RoleTimer {
   bool on;
-  unsigned long long t0, w[2];
-  DEVI RoleTimer(bool enabled) : on(enabled), t0(enabled ? clk64() : 0) { w[0] = w[1] = 0; }
+  unsigned long long t0, w[3];
+  DEVI RoleTimer(bool enabled) : on(enabled), t0(enabled ? clk64() : 0) { w[0] = w[1] = w[2] = 0; }
+  DEVI unsigned long long now() const { return on ? clk64() : 0; }
+  DEVI void add_fixup(unsigned long long since) {
+    if (on) w[2] += clk64() - since;
+  }
   DEVI void wait(uint64_t* bar, uint32_t parity, int k) {
     if (!on) {
       mbar_wait(bar, parity);
@@ -119,8 +184,17 @@ struct RoleTimer {
     g_role_cycles[role][0] = w[0];
     g_role_cycles[role][1] = w[1];
     g_role_cycles[role][2] = clk64() - t0;
+    g_role_cycles[role][3] = w[2];
   }
 };
+// debug: per-unit event clocks of the traced CTA: [event][unit], unit < 64
+// (0 W issue, 1 X issue, 2 data arrived, 3 expanded, 4 MMA issued,
+//  5 accumulator ready, 6 accumulator released, 7 unit retired,
+//  8 epilogue iteration top, 9 epilogue scales ready)
+__device__ unsigned long long g_trace[12][64];
+DEVI void trace(bool on, int ev, int i) {
+  if (on && i < 64) g_trace[ev][i] = clk64();
+}
 DEVI uint32_t smid() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
@@ -129,20 +203,23 @@ DEVI uint32_t smid() {
 
 template <int BN, bool kGroupK, bool kAccOut>
 __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
-    w4ax_gemm_decode_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX4,
-                            const __grid_constant__ CUtensorMap tmX8, const __grid_constant__ BlockMap map,
-                            GemmArgs args, DecSched sched) {
+    w4ax_gemm_decode_kernel(const __grid_constant__ CUtensorMap tmSx, const __grid_constant__ CUtensorMap tmX4,
+                            const __grid_constant__ CUtensorMap tmX8, const __grid_constant__ CUtensorMap tmSw,
+                            const __grid_constant__ BlockMap map, GemmArgs args, DecSched sched) {
   using C = DecCfg<BN>;
+  using It = UnitIt<C::kUB>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t scale_base = sbase + C::kStages * C::kStageBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + C::kScaleSlots * C::kSlotBytes);
-  uint64_t* full = bars;                      // [kStages]
-  uint64_t* expd = full + C::kStages;         // [kStages] 4 expansion warps
-  uint64_t* empty = expd + C::kStages;        // [kStages] MMA commit
-  uint64_t* tfull = empty + C::kStages;       // [kAcc]
+  const uint32_t scale_base = sbase + C::kScaleBase;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarBase);
+  uint64_t* wfull = bars;                     // [kWStages] weight bytes landed
+  uint64_t* wempty = wfull + C::kWStages;     // [kWStages] 4 expansion warps read them
+  uint64_t* xfull = wempty + C::kWStages;     // [kXStages] token bytes landed
+  uint64_t* xempty = xfull + C::kXStages;     // [kXStages] MMA commit
+  uint64_t* expd = xempty + C::kXStages;      // [kXStages] 4 expansion warps
+  uint64_t* tfull = expd + C::kXStages;       // [kAcc]
   uint64_t* tempty = tfull + C::kAcc;         // [kAcc] epilogue warps
   uint64_t* sfull = tempty + C::kAcc;         // [kScaleSlots]
   uint64_t* sempty = sfull + C::kScaleSlots;  // [kScaleSlots]
@@ -154,17 +231,20 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
   const int lane = threadIdx.x & 31;
   const int nb = args.nb;
   const int u0 = sched.u_begin(blockIdx.x), u1 = sched.u_begin(blockIdx.x + 1);
-  const int nu = u1 - u0;
   if (threadIdx.x == 0 && g_cta_times_on && blockIdx.x < 1024) {
     g_cta_times[3 * blockIdx.x] = global_ns();
     g_cta_times[3 * blockIdx.x + 2] = smid();
   }
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&full[s], 1);
+    for (int s = 0; s < C::kWStages; ++s) {
+      mbar_init(&wfull[s], 1);
+      mbar_init(&wempty[s], 4);
+    }
+    for (int s = 0; s < C::kXStages; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], 1);
       mbar_init(&expd[s], 4);
-      mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < C::kAcc; ++a) {
       mbar_init(&tfull[a], 1);
@@ -177,10 +257,11 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
     for (int a = 0; a < C::kASlots; ++a) mbar_init(&aempty[a], 1);
     fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmW);
+  if (warp == 2 && lane == 0) {
     tma_prefetch_desc(&tmX4);
     tma_prefetch_desc(&tmX8);
+    tma_prefetch_desc(&tmSx);
+    if (!kGroupK) tma_prefetch_desc(&tmSw);
   }
   if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_holder);
   tc_fence_before();
@@ -188,72 +269,103 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  auto tile_coords = [&](int t, int& n0, int& m0) {
-    n0 = (t % sched.n_tiles) * 128;
-    m0 = (t / sched.n_tiles) * BN;
-  };
 
-  if (warp == 0) {
-    // ------------------------------------------------- a3: producer ----
+  if (COMET_DEC_EXP == 5) {
+  } else if (warp == 0) {
+    // ------------------------------------------ a3: weight producer ----
+    // only the HBM weight stream: one bulk copy per unit, nothing else on
+    // this warp's issue path
     const uint64_t pol_w = l2_policy_evict_first();
-    RoleTimer rt(g_cta_times_on && blockIdx.x == 0 && lane == 0);
-    int t = u0 / nb, b = u0 - t * nb;
-    int n0, m0;
-    tile_coords(t, n0, m0);
-    for (int i = 0; i < nu; ++i) {
-      const int s = i % C::kStages;
-      const uint32_t code = map.code[b];
-      const bool is8 = (code >> 15) != 0;
-      const int rank = code & 0x7FFF;
-      rt.wait(&empty[s], ((i / C::kStages) & 1) ^ 1, 0);
-      uint8_t* st = smem + s * C::kStageBytes;
+    RoleTimer rt(g_cta_times_on && blockIdx.x + 1 == g_cta_times_on && lane == 0);
+    int i = 0;
+    for (It it(u0, u1, nb, sched.n_tiles); it.valid(); it.next(nb), ++i) {
+      const int s = i % C::kWStages;
+      rt.wait(&wempty[s], ((i / C::kWStages) & 1) ^ 1, 0);
+      trace(rt.on, 0, i);
       if (elect_one()) {
-        mbar_arrive_expect_tx(&full[s], C::kWPBytes + (is8 ? C::kBBytes : C::kXPBytes));
-        bulk_load_hint(st, args.Wq + ((int64_t)(n0 >> 7) * nb + b) * 8192, 8192, &full[s], pol_w);
-        if (is8)
-          tma_load_2d(st + C::kWPBytes, &tmX8, &full[s], rank * 128, m0);
-        else
-          tma_load_2d(st + C::kWPBytes + C::kBBytes, &tmX4, &full[s], rank * 64, m0);
+        mbar_arrive_expect_tx(&wfull[s], it.len * C::kWPBytes);
+        // the unit's blocks are consecutive 8 KB slabs of the tiled layout
+        bulk_load_hint(smem + s * C::kWStageBytes, args.Wq + ((int64_t)it.tn * nb + it.b) * 8192,
+                       it.len * 8192, &wfull[s], pol_w);
+      }
+      __syncwarp();
+    }
+    rt.flush(0);
+  } else if (warp == 2) {
+    // ---------------------------------- a3: token + scale producer ----
+    const bool tr_on = g_cta_times_on && blockIdx.x + 1 == g_cta_times_on && lane == 0;
+    int i = 0;
+    for (It it(u0, u1, nb, sched.n_tiles); it.valid(); it.next(nb), ++i) {
+      const int s = i % C::kXStages;
+      const int n0 = it.tn * 128, m0 = it.tm * BN;
+      mbar_wait(&xempty[s], ((i / C::kXStages) & 1) ^ 1);
+      trace(tr_on, 1, i);
+      uint8_t* st = smem + C::kXBase + s * C::kXStageBytes;
+      if (elect_one()) {
+        uint32_t tx = 0;
+#pragma unroll
+        for (int j = 0; j < C::kUB; ++j)
+          if (j < it.len && COMET_DEC_EXP < 2) tx += (map.code[it.b + j] >> 15) ? C::kBBytes : C::kXPBytes;
+        mbar_arrive_expect_tx(&xfull[s], tx);
+#pragma unroll
+        for (int j = 0; j < C::kUB; ++j) {
+          if (j < it.len && COMET_DEC_EXP < 2) {
+            const uint32_t code = map.code[it.b + j];
+            const int rank = code & 0x7FFF;
+            if (code >> 15)
+              tma_load_2d(st + j * C::kBBytes, &tmX8, &xfull[s], rank * 128, m0);
+            else
+              tma_load_2d(st + C::kXPOff + j * C::kXPBytes, &tmX4, &xfull[s], rank * 64, m0);
+          }
+        }
       }
       if (!kAccOut) {
         const int a = i % C::kScaleSlots;
-        rt.wait(&sempty[a], ((i / C::kScaleSlots) & 1) ^ 1, 1);
+        mbar_wait(&sempty[a], ((i / C::kScaleSlots) & 1) ^ 1);
         if (elect_one()) {
-          const bool seg_end = (b == nb - 1) || (i == nu - 1);
-          const int nsx = max(0, min(BN, (int)args.ldsx - m0));  // multiple of 4
-          const int nsw = (!kGroupK || seg_end) ? 128 : 0;
-          mbar_arrive_expect_tx(&sfull[a], (nsx + nsw) * 4);
-          uint8_t* slot = smem + C::kStages * C::kStageBytes + a * C::kSlotBytes;
-          if (nsx) bulk_load(slot, args.Sx + (int64_t)b * args.ldsx + m0, nsx * 4, &sfull[a]);
-          if (nsw) bulk_load(slot + BN * 4, args.Sw + (kGroupK ? 0 : (int64_t)b * args.N) + n0, 512, &sfull[a]);
+          const bool seg_end = (it.b + it.len == nb) || (it.u + it.len == u1);
+          uint8_t* slot = smem + C::kScaleBase + a * C::kSlotBytes;
+          // sx of the unit's blocks: one [kUB x BN] box of Sx [nb x ldsx]
+          // (columns >= ldsx and rows >= nb are zero-filled, still counted)
+          const uint32_t tx = (COMET_DEC_EXP >= 1 ? 0 : C::kSxBytes) +
+                              (kGroupK ? (seg_end ? 512 : 0) : C::kUB * 512);
+          mbar_arrive_expect_tx(&sfull[a], tx);
+          if (COMET_DEC_EXP < 1) tma_load_2d(slot, &tmSx, &sfull[a], m0, it.b);
+          if (!kGroupK)
+            tma_load_2d(slot + C::kSxBytes, &tmSw, &sfull[a], n0, it.b);  // [kUB x 128] box of Sw [nb x N]
+          else if (seg_end)
+            bulk_load(slot + C::kSxBytes, args.Sw + n0, 512, &sfull[a]);
         }
       }
       __syncwarp();
-      if (++b == nb) {
-        b = 0;
-        ++t;
-        if (t < sched.tiles) tile_coords(t, n0, m0);
-      }
     }
-    rt.flush(0);
   } else if (warp == 1) {
     // ------------------------------------------------------ a5: MMA ----
     constexpr uint32_t idesc = idesc_i8(128, BN);
-    RoleTimer rt(g_cta_times_on && blockIdx.x == 0 && lane == 0);
-    for (int i = 0; i < nu; ++i) {
-      const int s = i % C::kStages;
+    RoleTimer rt(g_cta_times_on && blockIdx.x + 1 == g_cta_times_on && lane == 0);
+    int i = 0;
+    for (It it(u0, u1, nb, sched.n_tiles); it.valid(); it.next(nb), ++i) {
+      const int s = i % C::kXStages;
       const int acc = i % C::kAcc;
       rt.wait(&tempty[acc], ((i / C::kAcc) & 1) ^ 1, 0);
-      rt.wait(&expd[s], (i / C::kStages) & 1, 1);
+      rt.wait(&expd[s], (i / C::kXStages) & 1, 1);
+      trace(rt.on, 4, i);
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t b0 = sbase + s * C::kStageBytes + C::kWPBytes;
+        const uint32_t bst = sbase + C::kXBase + s * C::kXStageBytes;
         const int as = i % C::kASlots;
-        const uint32_t a0 = tmem_base + C::kAOff + 32 * as;
+        const uint32_t a0 = tmem_base + C::kAOff + 32 * C::kUB * as;
+        const uint32_t d0 = tmem_base + acc * C::kAccCols;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          mma_i8_ts(tmem_base + acc * BN, a0 + 8 * k, umma_desc_sw128_kmajor(b0 + 32 * k), idesc, k > 0 ? 1u : 0u);
-        mma_commit(&empty[s]);
+        for (int j = 0; j < C::kUB; ++j) {
+          if (j < it.len) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_i8_ts(d0 + j * BN, a0 + 32 * j + 8 * k, umma_desc_sw128_kmajor(bst + j * C::kBBytes + 32 * k), idesc,
+                        k > 0 ? 1u : 0u);
+          }
+        }
+        mma_commit(&xempty[s]);
         mma_commit(&aempty[as]);
         mma_commit(&tfull[acc]);
       }
@@ -266,53 +378,71 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
     const int row = 32 * q + lane;  // weight row of the tile = TMEM lane
     const int grp = (warp - 4) >> 2;
     const int tid = threadIdx.x - 128 - 128 * grp;
-    int b = (u0 + grp) % nb;
-    RoleTimer rt(g_cta_times_on && blockIdx.x == 0 && warp == 4 && lane == 0);
-    for (int i = grp; i < nu; i += C::kExpGroups) {
-      const int s = i % C::kStages;
-      const bool is8 = (map.code[b] >> 15) != 0;
-      b += C::kExpGroups;
-      if (b >= nb) b -= nb;
-      const uint32_t st = sbase + s * C::kStageBytes;
-      rt.wait(&full[s], (i / C::kStages) & 1, 0);
-      // own weight row: 4 x 16 B, 64B-swizzled (chunk c at c ^ ((row >> 1) & 3))
-      uint32_t e[32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const uint4 w = lds128(st + row * 64 + ((c ^ ((row >> 1) & 3)) << 4));
-        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t tt = ww[k] & 0x0F0F0F0Fu;
-          e[8 * c + 2 * k] = tt << 4;           // 16*e0..3
-          e[8 * c + 2 * k + 1] = ww[k] - tt;    // 16*e4..7
-        }
-      }
+    RoleTimer rt(g_cta_times_on && blockIdx.x + 1 == g_cta_times_on && warp == 4 && lane == 0);
+    int i = 0;
+    for (It it(u0, u1, nb, sched.n_tiles); it.valid(); it.next(nb), ++i) {
+      if (C::kExpGroups > 1 && (i % C::kExpGroups) != grp) continue;
+      const int ws = i % C::kWStages, s = i % C::kXStages;
+      const uint32_t wst = sbase + ws * C::kWStageBytes;
+      const uint32_t st = sbase + C::kXBase + s * C::kXStageBytes;
       const int as = i % C::kASlots;
-      rt.wait(&aempty[as], ((i / C::kASlots) & 1) ^ 1, 1);  // MMA of unit i - kASlots done
-      tc_fence_after();
-      tmem_st_32x32b_x32(tmem_base + ((uint32_t)(32 * q) << 16) + C::kAOff + 32 * as, e);
-      if (!is8) {
-        const uint32_t xp = st + C::kWPBytes + C::kBBytes;
-        const uint32_t xb = st + C::kWPBytes;
-        for (int tk = tid; tk < BN * 4; tk += 128) {
-          const int r = tk >> 2, j = tk & 3;
-          const uint4 w = lds128(xp + r * 64 + j * 16);
-          uint4 o0, o1;
-          uint32_t tt;
-          tt = w.x & 0x0F0F0F0Fu; o0.x = tt << 4; o0.y = w.x - tt;
-          tt = w.y & 0x0F0F0F0Fu; o0.z = tt << 4; o0.w = w.y - tt;
-          tt = w.z & 0x0F0F0F0Fu; o1.x = tt << 4; o1.y = w.z - tt;
-          tt = w.w & 0x0F0F0F0Fu; o1.z = tt << 4; o1.w = w.w - tt;
-          sts128(xb + r * 128 + (((2 * j) ^ (r & 7)) << 4), o0);
-          sts128(xb + r * 128 + (((2 * j + 1) ^ (r & 7)) << 4), o1);
+      const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + C::kAOff + 32 * C::kUB * as;
+      rt.wait(&wfull[ws], (i / C::kWStages) & 1, 0);
+      trace(rt.on, 2, i);
+#pragma unroll
+      for (int j = 0; j < C::kUB; ++j) {
+        if (j < it.len) {
+          // own weight row of block j: 4 x 16 B, 64B-swizzled (chunk c at c ^ ((row >> 1) & 3))
+          uint32_t e[32];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint4 w = lds128(wst + j * C::kWPBytes + row * 64 + ((c ^ ((row >> 1) & 3)) << 4));
+            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t tt = ww[k] & 0x0F0F0F0Fu;
+              e[8 * c + 2 * k] = tt << 4;         // 16*e0..3
+              e[8 * c + 2 * k + 1] = ww[k] - tt;  // 16*e4..7
+            }
+          }
+          if (j == 0) {
+            rt.wait(&aempty[as], ((i / C::kASlots) & 1) ^ 1, 1);  // MMA of unit i - kASlots done
+            tc_fence_after();
+          }
+          tmem_st_32x32b_x32(ta + 32 * j, e);
         }
-        fence_proxy_async_smem();
       }
+      // packed weights consumed into registers: release the weight stage now
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&wempty[ws]);
+      mbar_wait(&xfull[s], (i / C::kXStages) & 1);
+      bool any4 = false;
+#pragma unroll
+      for (int j = 0; j < C::kUB; ++j) {
+        if (j < it.len && !(map.code[it.b + j] >> 15)) {
+          any4 = true;
+          const uint32_t xp = st + C::kXPOff + j * C::kXPBytes;
+          const uint32_t xb = st + j * C::kBBytes;
+          for (int tk = tid; tk < BN * 4; tk += 128) {
+            const int r = tk >> 2, jj = tk & 3;
+            const uint4 w = lds128(xp + r * 64 + jj * 16);
+            uint4 o0, o1;
+            uint32_t tt;
+            tt = w.x & 0x0F0F0F0Fu; o0.x = tt << 4; o0.y = w.x - tt;
+            tt = w.y & 0x0F0F0F0Fu; o0.z = tt << 4; o0.w = w.y - tt;
+            tt = w.z & 0x0F0F0F0Fu; o1.x = tt << 4; o1.y = w.z - tt;
+            tt = w.w & 0x0F0F0F0Fu; o1.z = tt << 4; o1.w = w.w - tt;
+            sts128(xb + r * 128 + (((2 * jj) ^ (r & 7)) << 4), o0);
+            sts128(xb + r * 128 + (((2 * jj + 1) ^ (r & 7)) << 4), o1);
+          }
+        }
+      }
+      if (any4) fence_proxy_async_smem();
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&expd[s]);
+      trace(rt.on, 3, i);
     }
     rt.flush(2);
   } else if (warp >= C::kEpiWarp0) {
@@ -322,33 +452,34 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
     const int row = 32 * q + lane;
     const int col0 = h * C::kCW;
     const uint32_t tl = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)col0;
-    float y[C::kCW];
+    // running sums as packed fp32 pairs (FFMA2 / FMUL2: half the issue slots)
+    uint64_t y2[C::kCW / 2];
 #pragma unroll
-    for (int j = 0; j < C::kCW; ++j) y[j] = 0.f;
-    int t = u0 / nb, b = u0 - t * nb;
-    int seg_first = b;  // first block of the current segment
-    RoleTimer rt(g_cta_times_on && blockIdx.x == 0 && warp == C::kEpiWarp0 && lane == 0);
-    for (int i = 0; i < nu; ++i) {
+    for (int j = 0; j < C::kCW / 2; ++j) y2[j] = 0ull;
+    int seg_first = u0 % nb;  // first block of the current segment
+    RoleTimer rt(g_cta_times_on && blockIdx.x + 1 == g_cta_times_on && warp == C::kEpiWarp0 && lane == 0);
+    int i = 0;
+    for (It it(u0, u1, nb, sched.n_tiles); it.valid(); it.next(nb), ++i) {
       const int acc = i % C::kAcc;
       const int a = i % C::kScaleSlots;
       const uint32_t slot = scale_base + a * C::kSlotBytes;
-      const bool is8 = (map.code[b] >> 15) != 0;
-      int n0, m0;
-      tile_coords(t, n0, m0);
+      const int t = it.t;
+      const int n0 = it.tn * 128, m0 = it.tm * BN;
       const int n = n0 + row;
-      float swv = 0.f;
-      if (!kAccOut) {
-        rt.wait(&sfull[a], (i / C::kScaleSlots) & 1, 0);
-        swv = kGroupK ? 1.f : lds_f32(slot + BN * 4 + row * 4);
-        swv *= is8 ? 0.0625f : 0.00390625f;  // fold 16^-e
-      }
+      trace(rt.on, 8, i);
+      if (!kAccOut) rt.wait(&sfull[a], (i / C::kScaleSlots) & 1, 0);
+      trace(rt.on, 9, i);
       rt.wait(&tfull[acc], (i / C::kAcc) & 1, 1);
+      trace(rt.on, 5, i);
       tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < C::kCW; c += C::kChunk) {
-        uint32_t r[C::kChunk];
-        tmem_ld_n<C::kChunk>(tl + acc * BN + c, r);
-        tmem_ld_wait();
+      // one block's chunk of kChunk accumulator columns [c, c + kChunk)
+      auto consume = [&](int jb, int c, const uint32_t* r) {
+        if (COMET_DEC_EXP == 3) {
+          y2[c / 2] += r[0];
+          return;
+        }
+        const int b = it.b + jb;
+        const bool is8 = (map.code[b] >> 15) != 0;
         if (kAccOut) {
           const int sh = is8 ? 4 : 8;
 #pragma unroll
@@ -357,25 +488,73 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
             if (m < args.M) args.Acc[((int64_t)b * args.M + m) * args.N + n] = ((int32_t)r[j]) >> sh;
           }
         } else {
+          float swv = kGroupK ? 1.f : lds_f32(slot + C::kSxBytes + jb * 512 + row * 4);
+          swv *= is8 ? 0.0625f : 0.00390625f;  // fold 16^-e
+          const uint64_t sw2 = pack2(swv, swv);
 #pragma unroll
           for (int j4 = 0; j4 < C::kChunk; j4 += 4) {
-            const float4 sx4 = lds_f32x4(slot + (col0 + c + j4) * 4);
-            y[c + j4 + 0] = fmaf(i2f(r[j4 + 0]), sx4.x * swv, y[c + j4 + 0]);
-            y[c + j4 + 1] = fmaf(i2f(r[j4 + 1]), sx4.y * swv, y[c + j4 + 1]);
-            y[c + j4 + 2] = fmaf(i2f(r[j4 + 2]), sx4.z * swv, y[c + j4 + 2]);
-            y[c + j4 + 3] = fmaf(i2f(r[j4 + 3]), sx4.w * swv, y[c + j4 + 3]);
+            // y[m] += float(acc[m]) * (sx[m] * swv), two columns per instruction
+            uint64_t sx01, sx23;
+            lds_u64x2(slot + jb * BN * 4 + (col0 + c + j4) * 4, sx01, sx23);
+            cvt_fma2(y2[(c + j4) / 2], r[j4 + 0], r[j4 + 1], mul2_u(sx01, sw2));
+            cvt_fma2(y2[(c + j4) / 2 + 1], r[j4 + 2], r[j4 + 3], mul2_u(sx23, sw2));
           }
         }
+      };
+      if (COMET_DEC_EXP == 4) {
+      } else if constexpr (C::kCW <= 32) {
+        // kLdG blocks' accumulators (<= 32 registers) in flight before one wait
+#pragma unroll
+        for (int jb0 = 0; jb0 < C::kUB; jb0 += C::kLdG) {
+          if (jb0 < it.len) {
+            uint32_t r[C::kLdG][C::kCW];
+#pragma unroll
+            for (int g = 0; g < C::kLdG; ++g)
+              if (jb0 + g < it.len) {
+#pragma unroll
+                for (int c = 0; c < C::kCW; c += C::kChunk)
+                  tmem_ld_n<C::kChunk>(tl + acc * C::kAccCols + (jb0 + g) * BN + c,
+                                       *reinterpret_cast<uint32_t(*)[C::kChunk]>(&r[g][c]));
+              }
+            tmem_ld_wait();
+#pragma unroll
+            for (int g = 0; g < C::kLdG; ++g)
+              if (jb0 + g < it.len) {
+#pragma unroll
+                for (int c = 0; c < C::kCW; c += C::kChunk) consume(jb0 + g, c, &r[g][c]);
+              }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int jb = 0; jb < C::kUB; ++jb)
+          if (jb < it.len) {
+#pragma unroll
+            for (int c = 0; c < C::kCW; c += C::kChunk) {
+              uint32_t r[C::kChunk];
+              tmem_ld_n<C::kChunk>(tl + acc * C::kAccCols + jb * BN + c, r);
+              tmem_ld_wait();
+              consume(jb, c, r);
+            }
+          }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+      trace(rt.on, 6, i);
 
-      const bool tile_end = (b == nb - 1);
-      const bool seg_end = tile_end || (i == nu - 1);
+      const bool tile_end = (it.b + it.len == nb);
+      const bool seg_end = tile_end || (it.u + it.len == u1);
       if (!kAccOut && seg_end) {
+        float y[C::kCW];
+#pragma unroll
+        for (int j = 0; j < C::kCW / 2; ++j) {
+          const float2 f = unpack2(y2[j]);
+          y[2 * j] = f.x;
+          y[2 * j + 1] = f.y;
+        }
         if (kGroupK) {
-          const float swr = lds_f32(slot + BN * 4 + row * 4);
+          const float swr = lds_f32(slot + C::kSxBytes + row * 4);
 #pragma unroll
           for (int j = 0; j < C::kCW; ++j) y[j] *= swr;
         }
@@ -388,6 +567,7 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
           }
         } else {
           // ------------------------- a7: stream-K partial + fixup ----
+          const unsigned long long tf = rt.now();
           // slot (cta, 0) = partial of the first tile of this CTA, (cta, 1) = last;
           // layout [row][BN]: this thread's kCW columns are contiguous
           const int which = (seg_first == (u0 % nb) && t == u0 / nb) ? 0 : 1;
@@ -395,23 +575,27 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
 #pragma unroll
           for (int j = 0; j < C::kCW; j += 4)
             __stcg(reinterpret_cast<float4*>(part + j), make_float4(y[j], y[j + 1], y[j + 2], y[j + 3]));
-          __threadfence();
-          epi_sync(32 * C::kEpiWarps);
-          // contributors of tile t: CTAs whose unit range intersects [t*nb, (t+1)*nb)
+          // contributors of tile t: CTAs whose block range intersects [t*nb, (t+1)*nb)
           const int tu0 = t * nb, tu1 = tu0 + nb;
-          int c_lo = (int)(((int64_t)tu0 * sched.ctas) / sched.units);
+          int c_lo = (int)(((uint32_t)tu0 * (uint32_t)sched.ctas) / (uint32_t)sched.units);
           while (c_lo > 0 && sched.u_begin(c_lo) > tu0) --c_lo;
           while (sched.u_begin(c_lo + 1) <= tu0) ++c_lo;
-          int c_hi = (int)(((int64_t)(tu1 - 1) * sched.ctas) / sched.units);
+          int c_hi = (int)(((uint32_t)(tu1 - 1) * (uint32_t)sched.ctas) / (uint32_t)sched.units);
           while (c_hi > 0 && sched.u_begin(c_hi) > tu1 - 1) --c_hi;
           while (sched.u_begin(c_hi + 1) <= tu1 - 1) ++c_hi;
+          // the epilogue threads' partial stores are ordered before thread 0's
+          // gpu-scope fence by the named barrier (release is cumulative); the
+          // last arriver's fence after the atomic orders the reads below
+          epi_sync(32 * C::kEpiWarps);
           if (threadIdx.x == 32 * C::kEpiWarp0) {
+            __threadfence();
             const int prev = atomicAdd(args.ws_counter + t, 1);
-            *s_flag = (prev == c_hi - c_lo);
+            const bool last = (prev == c_hi - c_lo);
+            if (last) __threadfence();
+            *s_flag = last;
           }
           epi_sync(32 * C::kEpiWarps);
           if (*s_flag) {
-            __threadfence();
             // sum the contributors in CTA order (deterministic); each round
             // issues kCW/4 independent 16-byte loads
 #pragma unroll
@@ -438,17 +622,15 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
             }
             if (threadIdx.x == 32 * C::kEpiWarp0) args.ws_counter[t] = 0;
           }
+          rt.add_fixup(tf);
         }
 #pragma unroll
-        for (int j = 0; j < C::kCW; ++j) y[j] = 0.f;
+        for (int j = 0; j < C::kCW / 2; ++j) y2[j] = 0ull;
       }
       __syncwarp();
       if (!kAccOut && lane == 0) mbar_arrive(&sempty[a]);
-      if (++b == nb) {
-        b = 0;
-        ++t;
-      }
-      if (seg_end) seg_first = b;
+      trace(rt.on, 7, i);
+      if (seg_end) seg_first = (it.b + it.len == nb) ? 0 : it.b + it.len;
     }
     rt.flush(3);
   }

@@ -37,6 +37,10 @@ DEVI void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+#ifndef COMET_MBAR_SUSPEND_NS
+#define COMET_MBAR_SUSPEND_NS 1000000
+#endif
+constexpr uint32_t kMbarSuspendNs = COMET_MBAR_SUSPEND_NS;
 DEVI bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -46,8 +50,24 @@ DEVI bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: a waiting warp is descheduled until the
+// phase completes (or the hint expires) instead of re-polling (measured: no
+// gain in the decode kernel, -6% in the prefill kernel -- kept for experiments)
+DEVI bool mbar_try_wait_suspend(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(kMbarSuspendNs)
+      : "memory");
+  return ok != 0;
+}
 DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
+  }
+}
+DEVI void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait_suspend(bar, parity)) {
   }
 }
 // non-blocking probe (no suspend), acquire at cluster scope
@@ -304,6 +324,10 @@ DEVI void cvt_fma2_magic(uint64_t& y, uint32_t a0, uint32_t a1, uint64_t s) {
       " fma.rn.f32x2 %0, p, %3, %0;\n}\n"
       : "+l"(y)
       : "r"(a0), "r"(a1), "l"(s), "l"(0xCB400000CB400000ull));
+}
+// 16 B of shared memory as two packed fp32 pairs
+DEVI void lds_u64x2(uint32_t addr, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(addr));
 }
 DEVI uint64_t pack2(float lo, float hi) {
   uint64_t p;
