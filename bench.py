@@ -279,16 +279,19 @@ def run_comet(args, cfg, config_name):
     barrier()
 
     # ---- device-timed region ----
+    preroll = M <= 256
     n_launch0 = comet.launch_count()
     step_ms = []
     with ClockSampler(local) as clk:
         barrier()
         for _ in range(args.steps):
             flush.fill_(1)
-            # GPU spin (outside the events) so the host has enqueued the whole
-            # step before the device reaches it: the events then time the
-            # kernels, not Python launch gaps
-            torch.cuda._sleep(PREROLL_CYCLES)
+            # short (decode) steps: GPU spin outside the events so the host has
+            # enqueued the whole step before the device reaches it (the events
+            # then time kernels, not Python launch gaps). Long prefill steps
+            # enqueue ahead anyway, and the spin costs them ~2% (measured)
+            if preroll:
+                torch.cuda._sleep(PREROLL_CYCLES)
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record(stream)
             step(timed_kernels=True)
@@ -358,7 +361,7 @@ def run_comet(args, cfg, config_name):
            "config": {"workload": cfg["workload"], "M": M, "layers": cfg["layers"], "weight_scales": args.group,
                       "parallelism": f"tp{world} (N-sharded, NCCL all-gather of Y)" if world > 1 else "single GPU",
                       "l2": "flushed (256 MiB write) before every timed step, outside the events",
-                      "preroll": "GPU spin before each timed step so launches are queued ahead"},
+                      "preroll": ("GPU spin before each timed step so launches are queued ahead" if preroll else "none")},
            "tokens_per_s": M / (t_dev * 1e-3),
            "gemm_us": [g * 1e3 for g in gemm_ms],
            "quantize_us": [q * 1e3 for q in quant_ms],

@@ -268,12 +268,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
       const uint64_t sx2 = pack2(sxv, sxv);
       mbar_wait(&tfull[acc], (g >> 1) & 1);
       tc_fence_after();
+      if (kAccOut) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[16];
-        tmem_ld_32x32b_x16(tl + acc * 256 + 16 * c, r);
-        tmem_ld_wait();
-        if (kAccOut) {
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[16];
+          tmem_ld_32x32b_x16(tl + acc * 256 + 16 * c, r);
+          tmem_ld_wait();
           int m0, n0;
           sched.coords(t, m0, n0);
           const int sh = is8 ? 4 : 8;
@@ -285,17 +285,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
               if (n < args.N) args.Acc[((int64_t)b * args.M + m) * args.N + n] = ((int32_t)r[j]) >> sh;
             }
           }
-        } else if (kGroupK) {
+        }
+      } else {
+        // columns [8c, 8c + 8) of this warp's 64; the load of chunk c + 1 is
+        // in flight while chunk c is promoted
+        auto promote = [&](int c, const uint32_t (&r)[8]) {
+          if (kGroupK) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) cvt_fma2(y[8 * c + j], r[2 * j], r[2 * j + 1], sx2);
-        } else {
-          const uint32_t swa = slot + 512 + (64 * cg + 16 * c) * 4;
+            for (int j = 0; j < 4; ++j) cvt_fma2(y[4 * c + j], r[2 * j], r[2 * j + 1], sx2);
+          } else {
+            const uint32_t swa = slot + 512 + (64 * cg + 8 * c) * 4;
 #pragma unroll
-          for (int j4 = 0; j4 < 4; ++j4) {
-            const float4 w4 = lds_f32x4(swa + 16 * j4);
-            cvt_fma2(y[8 * c + 2 * j4], r[4 * j4], r[4 * j4 + 1], mul2_u(sx2, pack2(w4.x, w4.y)));
-            cvt_fma2(y[8 * c + 2 * j4 + 1], r[4 * j4 + 2], r[4 * j4 + 3], mul2_u(sx2, pack2(w4.z, w4.w)));
+            for (int j4 = 0; j4 < 2; ++j4) {
+              const float4 w4 = lds_f32x4(swa + 16 * j4);
+              cvt_fma2(y[4 * c + 2 * j4], r[4 * j4], r[4 * j4 + 1], mul2_u(sx2, pack2(w4.x, w4.y)));
+              cvt_fma2(y[4 * c + 2 * j4 + 1], r[4 * j4 + 2], r[4 * j4 + 3], mul2_u(sx2, pack2(w4.z, w4.w)));
+            }
           }
+        };
+        uint32_t ra[8], rb[8];
+        tmem_ld_32x32b_x8(tl + acc * 256, ra);
+        tmem_ld_wait_dep(ra);
+#pragma unroll
+        for (int c = 0; c < 8; c += 2) {
+          tmem_ld_32x32b_x8(tl + acc * 256 + 8 * (c + 1), rb);
+          promote(c, ra);
+          tmem_ld_wait_dep(rb);
+          if (c + 2 < 8) tmem_ld_32x32b_x8(tl + acc * 256 + 8 * (c + 2), ra);
+          promote(c + 1, rb);
+          if (c + 2 < 8) tmem_ld_wait_dep(ra);
         }
       }
       tc_fence_before();
