@@ -104,6 +104,21 @@ bool make_map_f32(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows
   return r == CUDA_SUCCESS;
 }
 
+// 2-D fp16 tensor [rows x cols] (row stride ld elements), box [box_rows x box_cols]
+bool make_map_f16(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t ld, uint32_t box_cols,
+                  uint32_t box_rows, CUtensorMapSwizzle swz) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // ---- block map ------------------------------------------------------------
 bool build_block_map(const uint8_t* bits, int nb, BlockMap* map, int* n8, int* n4) {
   int r8 = 0, r4 = 0;
@@ -165,13 +180,18 @@ comet_status launch_gemm_2sm(const CUtensorMap& tmW, const CUtensorMap& tmX4, co
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes); });
   if (attr_err != cudaSuccess) return cuda_fail(attr_err);
+  // a8: Y [M x N] fp16 (row stride ldy), stored in 32-row x 64-column boxes
+  CUtensorMap tmY = tmX4;  // never dereferenced on the INT32 debug path
+  if (!kAcc && !make_map_f16(&tmY, args.Y, (uint64_t)args.N, (uint64_t)args.M, (uint64_t)args.ldy, 64, 32,
+                             CU_TENSOR_MAP_SWIZZLE_128B))
+    return COMET_ERR_CUDA;
   PairSched sched;
   sched.m_tiles = p.m_tiles;
   sched.n_tiles = p.n_tiles;
   sched.tiles = p.m_tiles * p.n_tiles;
   sched.clusters = sched.tiles < p.clusters ? sched.tiles : p.clusters;  // persistent: one cluster per SM pair
   dim3 grid(2 * sched.clusters, 1, 1);
-  kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(tmW, tmX4, tmX8, map, args, sched);
+  kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(tmY, tmX4, tmX8, map, args, sched);
   return check_launch();
 }
 

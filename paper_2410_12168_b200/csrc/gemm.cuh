@@ -27,4 +27,69 @@ struct GemmArgs {
   int splits;
 };
 
+// ---- debug instrumentation ------------------------------------------------
+// Per-CTA start/end stamps are always compiled (once per CTA). Per-role cycle
+// counters and per-step event traces exist only in a -DCOMET_TRACE build
+// (tools/gemm_sweep.py builds one): even disabled, their code in the hot loops
+// cost the prefill kernel ~9% (register pressure).
+#ifdef COMET_TRACE
+constexpr bool kTraceBuild = true;
+#else
+constexpr bool kTraceBuild = false;
+#endif
+// debug: per-CTA [start, end, smid] globaltimer stamps (comet_debug_cta_times)
+__device__ unsigned long long g_cta_times[3 * 1024];
+__device__ int g_cta_times_on;
+DEVI unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+DEVI unsigned long long clk64() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+  return t;
+}
+// debug: per-role cycles of CTA g_cta_times_on - 1:
+// [role][0..3] = wait A, wait B, total, stream-K fixup (epilogue)
+__device__ unsigned long long g_role_cycles[4][4];
+struct RoleTimer {
+  bool on;
+  unsigned long long t0, w[3];
+  DEVI RoleTimer(bool enabled) : on(kTraceBuild && enabled), t0(on ? clk64() : 0) { w[0] = w[1] = w[2] = 0; }
+  DEVI unsigned long long now() const { return on ? clk64() : 0; }
+  DEVI void add_fixup(unsigned long long since) {
+    if (on) w[2] += clk64() - since;
+  }
+  DEVI void wait(uint64_t* bar, uint32_t parity, int k) {
+    if (!on) {
+      mbar_wait(bar, parity);
+      return;
+    }
+    const unsigned long long a = clk64();
+    mbar_wait(bar, parity);
+    w[k] += clk64() - a;
+  }
+  DEVI void flush(int role) {
+    if (!on) return;
+    g_role_cycles[role][0] = w[0];
+    g_role_cycles[role][1] = w[1];
+    g_role_cycles[role][2] = clk64() - t0;
+    g_role_cycles[role][3] = w[2];
+  }
+};
+// debug: per-unit event clocks of the traced CTA: [event][unit], unit < 64
+// (0 W issue, 1 X issue, 2 data arrived, 3 expanded, 4 MMA issued,
+//  5 accumulator ready, 6 accumulator released, 7 unit retired,
+//  8 epilogue iteration top, 9 epilogue scales ready)
+__device__ unsigned long long g_trace[12][64];
+DEVI void trace(bool on, int ev, int i) {
+  if (kTraceBuild && on && i < 64) g_trace[ev][i] = clk64();
+}
+DEVI uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
 }  // namespace comet

@@ -41,7 +41,12 @@
 namespace comet {
 
 struct Gemm2Cfg {
-  static constexpr int kStages = 4;
+  // 3 stages: operands are resident well before use (L2 hits, one step of
+  // ~1800 cycles ahead), and the freed 48 KB hold the output staging below
+#ifndef COMET_PF_STAGES
+#define COMET_PF_STAGES 3
+#endif
+  static constexpr int kStages = COMET_PF_STAGES;
   static constexpr int kScaleSlots = 8;
   static constexpr int kABytes = 128 * 128;   // tokens int8, SW128 K-major
   static constexpr int kBBytes = 128 * 128;   // weights int8 (this CTA's half of N)
@@ -50,8 +55,18 @@ struct Gemm2Cfg {
   static constexpr int kStageBytes = kABytes + kBBytes + kXPBytes + kWPBytes;  // 48 KiB
   static constexpr int kSlotBytes = 128 * 4 + 256 * 4;                        // sx[128] + sw[256]
   static constexpr int kScaleBytes = kScaleSlots * kSlotBytes;
+  // a8: each compute warp stages its 32 x 64 fp16 output block (128B-swizzled)
+  // for one TMA tensor store
+  static constexpr int kYWarpBytes = 32 * 64 * 2;
+  static constexpr int kYBase = kStages * kStageBytes + kScaleBytes;  // 1024-aligned
+#ifndef COMET_PF_TMA_STORE
+#define COMET_PF_TMA_STORE 1
+#endif
+  static constexpr bool kTmaStore = COMET_PF_TMA_STORE;
+  static constexpr int kBarBase = kYBase + (kTmaStore ? 16 * kYWarpBytes : 0);
   static constexpr int kBarBytes = 256;
-  static constexpr int kSmemBytes = kStages * kStageBytes + kScaleBytes + kBarBytes + 1024;
+  static constexpr int kSmemBytes = kBarBase + kBarBytes + 1024;
+  static_assert(kYBase % 1024 == 0 && kSmemBytes <= 227 * 1024, "smem budget");
   static constexpr int kThreads = 576;  // warps 0-15 compute, 16 TMA producer, 17 MMA issuer
   static constexpr int kLoadWarp = 16;
   static constexpr int kMmaWarp = 17;
@@ -88,7 +103,7 @@ DEVI void expand_chunk(uint4 w, uint32_t dst0, uint32_t dst1) {
 
 template <bool kGroupK, bool kAccOut>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
-    w4ax_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX4,
+    w4ax_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmX4,
                          const __grid_constant__ CUtensorMap tmX8, const __grid_constant__ BlockMap map, GemmArgs args,
                          PairSched sched) {
   using C = Gemm2Cfg;
@@ -97,7 +112,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
   uint8_t* smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t scale_base = sbase + C::kStages * C::kStageBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + C::kScaleBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarBase);
   uint64_t* full = bars;                       // [kStages] local TMA tx
   uint64_t* expd = full + C::kStages;          // [kStages] leader: 2 CTAs x 16 compute warps
   uint64_t* empty = expd + C::kStages;         // [kStages] MMA commit (multicast)
@@ -133,7 +148,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
     fence_mbar_init();
   }
   if (warp == C::kLoadWarp && lane == 0) {
-    tma_prefetch_desc(&tmW);
+    if (!kAccOut) tma_prefetch_desc(&tmY);
     tma_prefetch_desc(&tmX4);
     tma_prefetch_desc(&tmX8);
   }
@@ -142,6 +157,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
   cluster_sync();  // barrier inits + TMEM allocation visible cluster-wide
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // debug trace of one CTA (comet_debug_cta_times(cta + 1)); see tools/gemm_sweep.py trace2
+  const bool tr_cta = g_cta_times_on && blockIdx.x + 1 == g_cta_times_on;
 
   if (warp == C::kLoadWarp) {
     // ------------------------------------------------- a3: producer ----
@@ -149,12 +166,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
     int m0 = 0, n0 = 0;
     sched.coords(t, m0, n0);
     for (int g = 0; g < steps; ++g) {
-      const int s = g & (C::kStages - 1);
+      const int s = g % C::kStages;
       const uint32_t code = map.code[b];
       const bool is8 = (code >> 15) != 0;
       const int rank = code & 0x7FFF;
       const int my_m0 = m0 + 128 * (int)crank;
       mbar_wait(&empty[s], ((g / C::kStages) & 1) ^ 1);
+      trace(tr_cta && lane == 0, 7, g);
       uint8_t* st = smem + s * C::kStageBytes;
       if (elect_one()) {
         // a half-populated pair tile (N % 256 == 128): the second CTA's weight
@@ -195,10 +213,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
     if (crank == 0) {
       constexpr uint32_t idesc = idesc_i8(256, 256);
       for (int g = 0; g < steps; ++g) {
-        const int s = g & (C::kStages - 1);
+        const int s = g % C::kStages;
         const int acc = g & 1;
         mbar_wait_cluster(&tempty[acc], ((g >> 1) & 1) ^ 1);
         mbar_wait_cluster(&expd[s], (g / C::kStages) & 1);
+        trace(tr_cta && lane == 0, 6, g);
         tc_fence_after();
         if (elect_one()) {
           const uint32_t a0 = sbase + s * C::kStageBytes;
@@ -223,11 +242,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
     const uint32_t leader_expd = mapa_shared(smem_u32(expd), 0);
     const uint32_t leader_tempty = mapa_shared(smem_u32(tempty), 0);
 
+    const bool tr_on = tr_cta && threadIdx.x == 0;
     // a4: expansion of global step j (block ex_b of its tile); this thread
     // handles packed row ct/4, 16-byte chunk ct%4 of both operands
     int ex_b = 0;
     auto expand = [&](int j) {
-      const int s = j & (C::kStages - 1);
+      const int s = j % C::kStages;
       const bool is8 = (map.code[ex_b] >> 15) != 0;
       if (++ex_b == nb) ex_b = 0;
       const uint32_t st = sbase + s * C::kStageBytes;
@@ -237,6 +257,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
       const uint32_t e_dst0 = er * 128 + (((2 * ej) ^ (er & 7)) << 4);
       const uint32_t e_dst1 = er * 128 + (((2 * ej + 1) ^ (er & 7)) << 4);
       mbar_wait(&full[s], (j / C::kStages) & 1);
+      trace(tr_on, 1, j);
       const uint4 w = lds128(st + C::kABytes + C::kBBytes + C::kXPBytes + w_src);
       if (!is8) {
         const uint4 x = lds128(st + C::kABytes + C::kBBytes + e_src);
@@ -246,6 +267,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_expd + s * 8);
+      trace(tr_on, 2, j);
     };
 
     uint64_t y[32];  // fp32 pairs (columns 2j, 2j+1 of this warp's 64)
@@ -254,6 +276,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
     int t = cluster, b = 0;
     if (steps > 0) expand(0);
     for (int g = 0; g < steps; ++g) {
+      trace(tr_on, 0, g);
       if (g + 1 < steps) expand(g + 1);
       // ---- a6: promote block b of tile t -----------------------------------
       const int acc = g & 1;
@@ -265,8 +288,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
         mbar_wait(&sfull[a], (g / C::kScaleSlots) & 1);
         sxv = lds_f32(slot + row * 4) * (is8 ? 0.0625f : 0.00390625f);  // fold 16^-e
       }
+      trace(tr_on, 3, g);
       const uint64_t sx2 = pack2(sxv, sxv);
       mbar_wait(&tfull[acc], (g >> 1) & 1);
+      trace(tr_on, 4, g);
       tc_fence_after();
       if (kAccOut) {
 #pragma unroll
@@ -319,6 +344,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_tempty + acc * 8);
+      trace(tr_on, 5, g);
 
       if (++b == nb) {
         // -------------------------------------------- a8: tile write-back ----
@@ -336,18 +362,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
               y[2 * j4 + 1] = mul2_u(y[2 * j4 + 1], pack2(w4.z, w4.w));
             }
           }
-          if (m < args.M && nbase < args.N) {
-            __half* yrow = args.Y + (int64_t)m * args.ldy + nbase;
+          if (!C::kTmaStore) {
+            if (m < args.M && nbase < args.N) {
+              __half* yrow = args.Y + (int64_t)m * args.ldy + nbase;
 #pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              __half2 h0 = __float22half2_rn(unpack2(y[4 * v + 0]));
-              __half2 h1 = __float22half2_rn(unpack2(y[4 * v + 1]));
-              __half2 h2 = __float22half2_rn(unpack2(y[4 * v + 2]));
-              __half2 h3 = __float22half2_rn(unpack2(y[4 * v + 3]));
-              uint4 pk = make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
-                                    *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
-              *reinterpret_cast<uint4*>(yrow + 8 * v) = pk;
+              for (int v = 0; v < 8; ++v) {
+                __half2 h0 = __float22half2_rn(unpack2(y[4 * v + 0]));
+                __half2 h1 = __float22half2_rn(unpack2(y[4 * v + 1]));
+                __half2 h2 = __float22half2_rn(unpack2(y[4 * v + 2]));
+                __half2 h3 = __float22half2_rn(unpack2(y[4 * v + 3]));
+                *reinterpret_cast<uint4*>(yrow + 8 * v) =
+                    make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                               *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
+              }
             }
+          } else {
+          // stage this warp's 32 rows x 64 columns (row = lane, 128 B, chunks
+          // 128B-swizzled: conflict-free) and hand it to one TMA store, which
+          // clips rows >= M and columns >= N
+          const uint32_t ybuf = sbase + C::kYBase + warp * C::kYWarpBytes;
+          if (lane == 0) bulk_wait_group_read0();  // previous tile's store has left smem
+          __syncwarp();
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            __half2 h0 = __float22half2_rn(unpack2(y[4 * v + 0]));
+            __half2 h1 = __float22half2_rn(unpack2(y[4 * v + 1]));
+            __half2 h2 = __float22half2_rn(unpack2(y[4 * v + 2]));
+            __half2 h3 = __float22half2_rn(unpack2(y[4 * v + 3]));
+            sts128(ybuf + lane * 128 + ((v ^ (lane & 7)) << 4),
+                   make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                              *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3)));
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmY, ybuf, nbase, m - lane);
+            bulk_commit_group();
+          }
           }
 #pragma unroll
           for (int j = 0; j < 32; ++j) y[j] = 0;
@@ -360,6 +411,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
     }
   }
 
+  if (C::kTmaStore && !kAccOut && warp < C::kNumEpiWarps && lane == 0) bulk_wait_group0();  // output stores complete
   tc_fence_before();
   __syncthreads();
   cluster_sync();

@@ -170,3 +170,23 @@ def trace(M, N, K, n8, cta=0, units=24):
     print("unit " + " ".join(f"{n:>7s}" for n in names))
     for i in range(units):
         print(f"{i:4d} " + " ".join(f"{a[e, i] - t0:7d}" for e in range(10)))
+
+
+def trace2(M, N, K, n8, cta=0, steps=40):
+    """prefill (CTA-pair) kernel: per-step event timeline of one CTA's compute warp 0"""
+    import ctypes
+    L = comet.lib()
+    L.comet_debug_cta_times.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
+    L.comet_debug_trace.argtypes = [ctypes.c_void_p]
+    buf = (ctypes.c_ulonglong * 768)()
+    L.comet_debug_cta_times(cta + 1, None, 0)
+    run(M, N, K, n8, "K", reps=1)
+    L.comet_debug_cta_times(0, None, 0)
+    L.comet_debug_trace(buf)
+    a = np.array(buf[:], dtype=np.int64).reshape(12, 64)
+    t0 = a[0, 0]
+    names = ["iter", "fullnx", "expdnx", "sxrdy", "accrdy", "promdn", "mma", "prod"]
+    print(f"M={M} N={N} K={K} CTA{cta} prefill trace (cycles rel. first iteration; fullnx/expdnx = step g):")
+    print("step " + " ".join(f"{n:>7s}" for n in names))
+    for i in range(steps):
+        print(f"{i:4d} " + " ".join(f"{a[e, i] - t0:7d}" for e in range(8)))

@@ -1,2 +1,5 @@
 #!/bin/bash
-python tools/gemm_sweep.py '[[16, 4096, 4096, 3], [16, 11008, 4096, 3], [16, 57344, 8192, 6], [16, 8192, 28672, 22], [1, 4096, 4096, 3], [64, 4096, 4096, 3], [128, 11008, 4096, 3]]' read 2>&1 | tail -7
+mkdir -p gpurun_out
+python -c "
+import sys; sys.path.insert(0, 'tools'); import gemm_sweep as g
+g.trace2(4096, 4096, 4096, 3, cta=0, steps=48)" > gpurun_out/trace2.txt 2>&1
