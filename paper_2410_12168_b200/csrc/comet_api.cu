@@ -12,6 +12,7 @@
 #include "../../include/comet.h"
 #include "gemm.cuh"
 #include "gemm_2sm.cuh"
+#include "gemm_pf.cuh"
 #include "gemm_decode.cuh"
 #include "quantize.cuh"
 
@@ -195,6 +196,29 @@ comet_status launch_gemm_2sm(const CUtensorMap& tmW, const CUtensorMap& tmX4, co
   return check_launch();
 }
 
+template <bool kGroupK, bool kAcc>
+comet_status launch_gemm_pf(const CUtensorMap& tmX4, const CUtensorMap& tmX8, const BlockMap& map,
+                            const GemmArgs& args, const Plan& p, cudaStream_t st) {
+  using C = PfCfg;
+  auto kern = w4ax_gemm_pf_kernel<kGroupK, kAcc>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes); });
+  if (attr_err != cudaSuccess) return cuda_fail(attr_err);
+  // a8: Y [M x N] fp16 (row stride ldy), stored in 32-row x 16-column boxes
+  CUtensorMap tmY = tmX4;  // never dereferenced on the INT32 debug path
+  if (!kAcc && !make_map_f16(&tmY, args.Y, (uint64_t)args.N, (uint64_t)args.M, (uint64_t)args.ldy, 16, 32,
+                             CU_TENSOR_MAP_SWIZZLE_NONE))
+    return COMET_ERR_CUDA;
+  PfSched sched;
+  sched.m_tiles = p.m_tiles;
+  sched.tiles = p.m_tiles * ((args.N + C::kTileN - 1) / C::kTileN);
+  sched.clusters = sched.tiles < p.clusters ? sched.tiles : p.clusters;
+  dim3 grid(2 * sched.clusters, 1, 1);
+  kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(tmY, tmX4, tmX8, map, args, sched);
+  return check_launch();
+}
+
 struct DecMaps {
   CUtensorMap sx, sw;  // Sx [nb x ldsx] box [kUB x BN]; Sw [nb x N] box [kUB x 128] (group 128)
 };
@@ -244,10 +268,24 @@ comet_status launch_decode_bn(const CUtensorMap& tmX4, const CUtensorMap& tmX8, 
   }
 }
 
+// prefill kernel selection: the TMEM-A kernel (gemm_pf.cuh) unless
+// COMET_PREFILL=2sm asks for the SMEM-operand CTA-pair kernel (A/B testing)
+bool use_pf() {
+  static const bool pf = [] {
+    const char* e = getenv("COMET_PREFILL");
+    return !(e && strcmp(e, "2sm") == 0);
+  }();
+  return pf;
+}
+
 template <bool kAcc>
 comet_status launch_gemm(const CUtensorMap& tmW, const CUtensorMap& tmX4, const CUtensorMap& tmX8,
                          const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
   const bool group_k = args.group_blocks == args.nb;
+  if (p.two_sm && use_pf()) {
+    if (group_k) return launch_gemm_pf<true, kAcc>(tmX4, tmX8, map, args, p, st);
+    return launch_gemm_pf<false, kAcc>(tmX4, tmX8, map, args, p, st);
+  }
   if (p.two_sm) {
     if (group_k) return launch_gemm_2sm<true, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
     return launch_gemm_2sm<false, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
@@ -288,8 +326,10 @@ comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, in
   if (!make_map_u8(&tmW, Wq, (uint64_t)K / 2, (uint64_t)N, (uint64_t)K / 2, 64, 128, CU_TENSOR_MAP_SWIZZLE_NONE))
     return COMET_ERR_CUDA;
   if (n4) {
+    // the TMEM-A prefill kernel reads packed token rows per thread: 64B swizzle
+    // keeps those 16-byte loads conflict-free
     if (!make_map_u8(&tmX4, Xq4, (uint64_t)n4 * 64, (uint64_t)M, (uint64_t)n4 * 64, 64, p.bn,
-                     CU_TENSOR_MAP_SWIZZLE_NONE))
+                     (p.two_sm && use_pf()) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE))
       return COMET_ERR_CUDA;
   } else {
     tmX4 = tmW;  // never dereferenced

@@ -1,0 +1,499 @@
+// gemm_pf.cuh -- prefill W4Ax GEMM (M > 128 tokens) on CTA pairs
+// (tcgen05 cta_group::2), persistent over pair tiles, tokens as the TMEM A
+// operand.
+//
+// Pair tile: 256 tokens (MMA M; 128 TMEM lanes in each CTA) x 192 weight rows
+// (each CTA stages 96 of them in smem).  K is walked one 128-channel FMPQ
+// block at a time.  Each block is issued as two N=96
+// "items" (the two 48-row halves of each CTA's weight rows), each into one of
+// four 96-column INT32 accumulators, so the promotion of item i overlaps the
+// MMAs of items i+1..i+3 (the paper's two-level overlap of conversion and
+// MMA, re-cut for TMEM).
+//
+// Roles per CTA (16 warps = 512 threads: the register file gives every
+// thread 128 registers, 64 of which hold the promotion's fp32 running sums):
+//   warps 12-15 (a4 staging; thread = token row of the warp's TMEM lane
+//       quarter): per block the row's token block -- zero-extended INT4 (x16,
+//       P:L294) or raw INT8 -- goes from smem through registers into the
+//       block's TMEM A slot (tcgen05.st), and 3 chunks of the packed weight
+//       rows are zero-extended into the SW128 K-major B operand in smem;
+//     warp 12 also is the producer (a3): kLoadAhead blocks ahead, 1-D bulk
+//       copies of the CTA's 96 packed weight rows (tiled layout, 64B swizzle
+//       baked in), a TMA of the token slab (INT8 blocks [128 x 128 B] SW128,
+//       INT4 blocks packed [128 x 64 B] SW64), 1-D copies of the scales;
+//     warp 13 of the leader also issues the MMAs (a5), kMmaLag blocks behind
+//       its staging: per item 4 x tcgen05.mma.cta_group::2.kind::i8 (A from
+//       TMEM, M=256, N=96, K=32) into a fresh accumulator, commit multicast;
+//   warps 0-11 (a6, a8; thread = token row): promote 2 x 32 columns of each
+//       block (16-column units 2k, 2k+1 of both items, k = warp / 4):
+//       tcgen05.ld of 32 columns, I2F, fma.rn.f32x2 with the thread-uniform
+//       row scale; per-channel weight scales are applied once per tile; at
+//       the tile's last block fp16 RNE -> smem -> TMA tensor stores.
+#pragma once
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "gemm.cuh"
+#include "gemm_2sm.cuh"
+#include "quantize.cuh"
+#include "sm100.cuh"
+
+namespace comet {
+
+// leader CTA only: D[tmem, both CTAs] (+)= A[tmem, both] . B[smem, both]^T
+DEVI void mma_i8_ts_2sm(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+#ifndef COMET_TRACE_EV2
+#define COMET_TRACE_EV2 0  // trace builds: events 6/9/10 = token-staging sub-steps instead of MMA/producer
+#endif
+constexpr bool kTraceEv2 = COMET_TRACE_EV2;
+
+#ifndef COMET_PF_FMAPIPE
+#define COMET_PF_FMAPIPE 0  // of every 4 column pairs, this many convert on the FMA pipe
+#endif
+
+struct PfCfg {
+  static constexpr int kTileN = 192;          // weight rows per pair tile
+  static constexpr int kRows = kTileN / 2;    // weight rows per CTA
+  static constexpr int kItemN = kTileN / 2;   // MMA N of one item (48 rows from each CTA)
+  static constexpr int kStages = 4;           // weight stages == TMEM A slots
+  static constexpr int kXStages = 3;          // token staging
+  static constexpr int kAccs = 4;             // 96-column accumulators
+  static constexpr int kScaleSlots = 8;
+  static constexpr int kWPBytes = kRows * 64;   // packed weights
+  static constexpr int kWEBytes = kRows * 128;  // expanded weights, SW128 K-major
+  static constexpr int kWStageBytes = kWEBytes + kWPBytes;  // 18 KB
+  static constexpr int kXStageBytes = 128 * 128;  // INT8 [128 x 128] or packed INT4 [128 x 64]
+  static constexpr int kXBase = kStages * kWStageBytes;
+  static constexpr int kScaleBase = kXBase + kXStages * kXStageBytes;
+  static constexpr int kSwOff = 512;                             // sx[128] then sw[192]
+  static constexpr int kSlotBytes = kSwOff + kTileN * 4;
+  static constexpr int kYBoxBytes = 32 * 16 * 2;                 // 32 rows x 16 fp16
+  static constexpr int kYBase = kScaleBase + kScaleSlots * kSlotBytes;
+  static constexpr int kBarBase = kYBase + 12 * 4 * kYBoxBytes;  // 12 promotion warps x 4 boxes
+  static constexpr int kBarBytes = 512;
+  static constexpr int kSmemBytes = kBarBase + kBarBytes + 1024;
+  static_assert(kWStageBytes % 1024 == 0 && kXBase % 1024 == 0, "SW128 operands need 1 KB alignment");
+  static_assert(kScaleBase % 16 == 0 && kYBase % 128 == 0, "alignment");
+  static_assert(kSmemBytes <= 227 * 1024, "smem budget");
+  static constexpr int kAccCols = kItemN;
+  static constexpr int kAOff = kAccs * kAccCols;  // TMEM A slots after the accumulators
+  static_assert(kAOff + 32 * kStages <= 512, "TMEM budget");
+  static constexpr int kThreads = 576;
+  static constexpr int kLoadWarp = 16;
+  static constexpr int kMmaWarp = 17;
+  static constexpr int kReadyCount = 2 * 4;         // both CTAs' staging warps
+  static constexpr int kTemptyCount = 2 * 12;       // both CTAs' promotion warps
+};
+
+struct PfSched {
+  int m_tiles, tiles, clusters;
+  DEVI void coords(int t, int& m0, int& n0) const {
+    const int mt = t % m_tiles;  // token tiles fastest: concurrent clusters share weight tiles
+    m0 = mt * 256;
+    n0 = (t / m_tiles) * PfCfg::kTileN;
+  }
+};
+
+// tile-relative weight column of item column j (0..95) of item h:
+// j < 48 -> CTA0's row 48h + j, else CTA1's row 48h + j - 48
+__host__ __device__ constexpr int pf_col(int h, int j) { return j < 48 ? 48 * h + j : PfCfg::kRows + 48 * h + j - 48; }
+
+template <bool kGroupK, bool kAccOut>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
+    w4ax_gemm_pf_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmX4,
+                        const __grid_constant__ CUtensorMap tmX8, const __grid_constant__ BlockMap map, GemmArgs args,
+                        PfSched sched) {
+  using C = PfCfg;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t scale_base = sbase + C::kScaleBase;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarBase);
+  uint64_t* wfull = bars;                        // [kStages] packed weights landed (tx)
+  uint64_t* wempty = wfull + C::kStages;         // [kStages] MMAs of the block done (commit multicast)
+  uint64_t* ready = wempty + C::kStages;         // [kStages] leader: operands of the block staged
+  uint64_t* xfull = ready + C::kStages;          // [kXStages] tokens landed (tx)
+  uint64_t* xempty = xfull + C::kXStages;        // [kXStages] 4 staging warps
+  uint64_t* tfull = xempty + C::kXStages;        // [kAccs] item's MMAs done (commit multicast)
+  uint64_t* tempty = tfull + C::kAccs;           // [kAccs] leader: 2 CTAs x 12 promotion warps
+  uint64_t* sfull = tempty + C::kAccs;           // [kScaleSlots] scales landed (tx)
+  uint64_t* sempty = sfull + C::kScaleSlots;     // [kScaleSlots] 12 promotion warps
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sempty + C::kScaleSlots);
+
+  // warp index via shfl from lane 0: ptxas then treats it (and everything
+  // derived from it) as warp-uniform
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const int cluster = blockIdx.x >> 1;
+  const int nb = args.nb;
+  const int my_tiles = cluster < sched.tiles ? (sched.tiles - 1 - cluster) / sched.clusters + 1 : 0;
+  const int steps = my_tiles * nb;  // (tile, block) steps of this cluster
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&wfull[s], 1);
+      mbar_init(&wempty[s], 1);
+      mbar_init(&ready[s], C::kReadyCount);
+    }
+    for (int x = 0; x < C::kXStages; ++x) {
+      mbar_init(&xfull[x], 1);
+      mbar_init(&xempty[x], 4);
+    }
+    for (int a = 0; a < C::kAccs; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], C::kTemptyCount);
+    }
+    for (int a = 0; a < C::kScaleSlots; ++a) {
+      mbar_init(&sfull[a], 1);
+      mbar_init(&sempty[a], 12);
+    }
+    fence_mbar_init();
+  }
+  if (warp == C::kLoadWarp && lane == 0) {
+    if (!kAccOut) tma_prefetch_desc(&tmY);
+    tma_prefetch_desc(&tmX4);
+    tma_prefetch_desc(&tmX8);
+  }
+  if (warp == C::kMmaWarp) tmem_alloc_2sm<512>(tmem_holder);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  // debug trace of one CTA (COMET_TRACE builds; tools/gemm_sweep.py trace3)
+  const bool tr_cta = kTraceBuild && g_cta_times_on && blockIdx.x + 1 == g_cta_times_on;
+
+  if (warp == C::kLoadWarp) {
+    // ------------------------------------------------- a3: producer ----
+    int pg = 0, pt = cluster, pb = 0, pm0 = 0, pn0 = 0;
+    sched.coords(pt, pm0, pn0);
+    for (; pg < steps;) {
+      const int g = pg, b = pb;
+      const int s = g % C::kStages, x = g % C::kXStages;
+      const int a = g & (C::kScaleSlots - 1);
+      // weights: stage s is free once the MMAs of block g - kStages are done
+      mbar_wait(&wempty[s], ((g / C::kStages) & 1) ^ 1);
+      mbar_wait(&xempty[x], ((g / C::kXStages) & 1) ^ 1);
+      if (!kAccOut) mbar_wait(&sempty[a], ((g / C::kScaleSlots) & 1) ^ 1);
+      const uint32_t code = map.code[b];
+      const bool is8 = (code >> 15) != 0;
+      const int rank = code & 0x7FFF;
+      const int my_m0 = pm0 + 128 * (int)crank;
+      if (elect_one()) {
+        // this CTA's weight rows [R, R + v) of the tile (v < 96 at the right
+        // edge of N); in the tiled layout they are contiguous within each
+        // 128-row slab
+        const int R = pn0 + C::kRows * (int)crank;
+        const int v = max(0, min(C::kRows, args.N - R));
+        mbar_arrive_expect_tx(&wfull[s], v * 64);
+        uint8_t* dst = smem + s * C::kWStageBytes + C::kWEBytes;
+        int r = R, left = v;
+        while (left > 0) {
+          const int in_slab = min(left, 128 - (r & 127));
+          bulk_load(dst, args.Wq + ((int64_t)(r >> 7) * nb + b) * 8192 + (r & 127) * 64, in_slab * 64, &wfull[s]);
+          dst += in_slab * 64;
+          r += in_slab;
+          left -= in_slab;
+        }
+        uint8_t* xs = smem + C::kXBase + x * C::kXStageBytes;
+        mbar_arrive_expect_tx(&xfull[x], is8 ? 128 * 128 : 128 * 64);
+        if (is8)
+          tma_load_2d(xs, &tmX8, &xfull[x], rank * 128, my_m0);
+        else
+          tma_load_2d(xs, &tmX4, &xfull[x], rank * 64, my_m0);
+        if (!kAccOut) {
+          const int nsx = max(0, min(128, (int)args.ldsx - my_m0));  // multiple of 4
+          const bool load_sw = !kGroupK || b == nb - 1;
+          const int nsw = load_sw ? max(0, min(C::kTileN, args.N - pn0)) : 0;  // multiple of 64
+          mbar_arrive_expect_tx(&sfull[a], (nsx + nsw) * 4);
+          uint8_t* slot = smem + C::kScaleBase + a * C::kSlotBytes;
+          if (nsx) bulk_load(slot, args.Sx + (int64_t)b * args.ldsx + my_m0, nsx * 4, &sfull[a]);
+          if (nsw)
+            bulk_load(slot + C::kSwOff, args.Sw + (kGroupK ? 0 : (int64_t)b * args.N) + pn0, nsw * 4, &sfull[a]);
+        }
+        trace(!kTraceEv2 && tr_cta, 9, g);
+      }
+      __syncwarp();
+      ++pg;
+      if (++pb == nb) {
+        pb = 0;
+        pt += sched.clusters;
+        if (pt < sched.tiles) sched.coords(pt, pm0, pn0);
+      }
+    }
+
+  } else if (warp == C::kMmaWarp) {
+    // --------------------------------------------- a5: MMA (leader) ----
+    // a5: MMA items (two N=96 items per block), issued in order when the
+    // block is staged and the item's accumulator is free (never blocks)
+    constexpr uint32_t idesc = idesc_i8(256, C::kItemN);
+    for (int i = 0; i < 2 * steps && crank == 0; ++i) {
+      const int g = i >> 1, h = i & 1;
+      const int s = g % C::kStages, acc = i % C::kAccs;
+      if (h == 0) mbar_wait_cluster(&ready[s], (g / C::kStages) & 1);
+      mbar_wait_cluster(&tempty[acc], ((i / C::kAccs) & 1) ^ 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t a_tm = tmem_base + C::kAOff + 32 * s;
+        const uint32_t bst = sbase + s * C::kWStageBytes;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mma_i8_ts_2sm(tmem_base + acc * C::kAccCols, a_tm + 8 * k,
+                        umma_desc_sw128_kmajor(bst + h * 48 * 128 + 32 * k), idesc, k > 0 ? 1u : 0u);
+        mma_commit_2sm(&tfull[acc], 0x3);
+        if (h == 1) mma_commit_2sm(&wempty[s], 0x3);
+        trace(tr_cta, 7 + h, g);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 12) {
+    // ---- warps 12-15: a4 staging (thread = token row of lane quarter q) ----
+    const int q = warp & 3;
+    const int et = threadIdx.x - 384;  // 0..127
+    const uint32_t tst = tmem_base + ((uint32_t)(32 * q) << 16) + C::kAOff;
+    const uint32_t leader_ready = mapa_shared(smem_u32(ready), 0);
+    int sb = 0;
+    for (int j = 0; j < steps; ++j) {
+      // ---- a4: stage block j (slot s: the producer waited for wempty[s]
+      // before the weight copy that completes wfull[s]) ----
+      const int x = j % C::kXStages, s = j % C::kStages;
+      const bool is8 = (map.code[sb] >> 15) != 0;
+      if (++sb == nb) sb = 0;
+      const uint32_t xs = sbase + C::kXBase + x * C::kXStageBytes;
+      const uint32_t wst = sbase + s * C::kWStageBytes;
+      mbar_wait(&xfull[x], (j / C::kXStages) & 1);
+      mbar_wait(&wfull[s], (j / C::kStages) & 1);
+      trace(tr_cta && threadIdx.x == 384, 10, j);
+      tc_fence_after();
+      // all shared-memory loads of the block first (the loads and stores are
+      // volatile asm, kept in program order: interleaving them would expose
+      // one load latency per chunk)
+      const uint32_t r_ = (32 * q) + (opaque(threadIdx.x) & 31);  // this thread's token row
+      uint4 tv[8];
+      if (is8) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) tv[c] = lds128(xs + r_ * 128 + ((c ^ (r_ & 7)) << 4));
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tv[c] = lds128(xs + r_ * 64 + ((c ^ ((r_ >> 1) & 3)) << 4));
+      }
+      uint4 wv[C::kRows * 4 / 128];
+#pragma unroll
+      for (int k = 0; k < C::kRows * 4 / 128; ++k) {
+        const int ch = et + 128 * k;
+        const int er = ch >> 2, ej = ch & 3;
+        wv[k] = lds128(wst + C::kWEBytes + er * 64 + ((ej ^ ((er >> 1) & 3)) << 4));
+      }
+      // tokens: 4 chunks of 32 K = 32 TMEM A columns (INT8 raw, INT4 x16)
+      {
+        uint32_t e[32];
+        if (is8) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            e[4 * c] = tv[c].x; e[4 * c + 1] = tv[c].y; e[4 * c + 2] = tv[c].z; e[4 * c + 3] = tv[c].w;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            zext_word(tv[c].x, e[8 * c + 0], e[8 * c + 1]);
+            zext_word(tv[c].y, e[8 * c + 2], e[8 * c + 3]);
+            zext_word(tv[c].z, e[8 * c + 4], e[8 * c + 5]);
+            zext_word(tv[c].w, e[8 * c + 6], e[8 * c + 7]);
+          }
+        }
+        tmem_st_32x32b_x32(tst + 32 * s, e);
+      }
+      // the token stage may be refilled once every lane's loads have landed
+      // (the tcgen05.st above consumed them; an arrive right after the LDS
+      // instructions could overtake them)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&xempty[x]);
+      trace(kTraceEv2 && tr_cta && threadIdx.x == 384, 6, j);
+      // weights: chunks et, et + 128, et + 256 of the packed slab -> SW128 B operand
+#pragma unroll
+      for (int k = 0; k < C::kRows * 4 / 128; ++k) {
+        const int ch = et + 128 * k;
+        const int er = ch >> 2, ej = ch & 3;
+        expand_chunk(wv[k], wst + er * 128 + (((2 * ej) ^ (er & 7)) << 4), wst + er * 128 + (((2 * ej + 1) ^ (er & 7)) << 4));
+      }
+      trace(kTraceEv2 && tr_cta && threadIdx.x == 384, 9, j);
+      fence_proxy_async_smem();
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_ready + s * 8);
+      trace(tr_cta && threadIdx.x == 384, 1, j);
+    }
+  } else {
+    // ------------------------ warps 0-11: a6 promotion + a8 write-back ----
+    const int q = warp & 3;         // TMEM lane quarter
+    const int kw = warp >> 2;       // 0..2: item units 2kw, 2kw+1 (columns [32kw, 32kw + 32))
+    const int row = 32 * q + lane;  // token row within this CTA
+    const uint32_t tl = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * kw);
+    const uint32_t leader_tempty = mapa_shared(smem_u32(tempty), 0);
+
+    uint64_t y[32];  // [item h][unit u][8 pairs]: columns 32kw + 16u + 2p (+1) of item h
+#pragma unroll
+    for (int j = 0; j < 32; ++j) y[j] = 0;
+    int t = cluster, b = 0;
+    // this row's activation scale of block g (x 16^-e_g), fetched one block
+    // ahead so its barrier wait and load latency overlap the promotion
+    auto fetch_sx = [&](int g, int bb) -> float {
+      if (kAccOut || g >= steps) return 0.f;
+      const int a = g & (C::kScaleSlots - 1);
+      mbar_wait(&sfull[a], (g / C::kScaleSlots) & 1);
+      const bool is8 = (map.code[bb] >> 15) != 0;
+      return lds_f32(scale_base + a * C::kSlotBytes + row * 4) * (is8 ? 0.0625f : 0.00390625f);
+    };
+    float sx_next = fetch_sx(0, 0);
+    const uint32_t one = opaque(1u);
+    for (int g = 0; g < steps; ++g) {
+      trace(tr_cta && threadIdx.x == 0, 0, g);
+      const int a = g & (C::kScaleSlots - 1);
+      const uint32_t slot = scale_base + a * C::kSlotBytes;
+      const bool is8 = (map.code[b] >> 15) != 0;
+      const float sxv = sx_next;
+      trace(tr_cta && threadIdx.x == 0, 11, g);
+      const uint64_t sx2 = pack2(sxv, sxv);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = 2 * g + h;
+        const int acc = i % C::kAccs;
+        mbar_wait(&tfull[acc], (i / C::kAccs) & 1);
+        trace(tr_cta && threadIdx.x == 0, 2 + 2 * h, g);
+        tc_fence_after();
+        const uint32_t ta = tl + acc * C::kAccCols;
+        if (kAccOut) {
+          int m0, n0;
+          sched.coords(t, m0, n0);
+          const int sh = is8 ? 4 : 8;
+          const int m = m0 + 128 * (int)crank + row;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            uint32_t r[16];
+            tmem_ld_32x32b_x16(ta + 16 * u, r);
+            tmem_ld_wait();
+            if (m < args.M) {
+              const int nu = n0 + pf_col(h, 32 * kw + 16 * u);
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (nu + j < args.N) args.Acc[((int64_t)b * args.M + m) * args.N + nu + j] = ((int32_t)r[j]) >> sh;
+            }
+          }
+        } else {
+          // 16 columns per tcgen05.ld (the running sums leave room for 16);
+          // the accumulator is released as soon as its last load has landed
+#pragma unroll
+          for (int c2 = 0; c2 < 2; ++c2) {
+            uint32_t r[16];
+            tmem_ld_32x32b_x16(ta + 16 * c2, r);
+            tmem_ld_wait();
+            if (c2 == 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive_cluster(leader_tempty + acc * 8);
+            }
+#pragma unroll
+            for (int c1 = 0; c1 < 2; ++c1) {  // 8-column chunks of this warp's 32 columns
+              const int c = 2 * c2 + c1;
+              uint64_t* yy = &y[16 * h + 4 * c];
+              if (kGroupK) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  if (j < COMET_PF_FMAPIPE)  // exact: |acc'| < 2^22 (SURVEY 7.3-1 iii)
+                    cvt_fma2_fmapipe(yy[j], r[8 * c1 + 2 * j], r[8 * c1 + 2 * j + 1], sx2, one);
+                  else
+                    cvt_fma2(yy[j], r[8 * c1 + 2 * j], r[8 * c1 + 2 * j + 1], sx2);
+                }
+              } else {
+                // group 128: this block's weight scales of the chunk's 8 columns
+                const uint32_t swa = slot + C::kSwOff + pf_col(h, 32 * kw + 8 * c) * 4;
+#pragma unroll
+                for (int j4 = 0; j4 < 2; ++j4) {
+                  const float4 w4 = lds_f32x4(swa + 16 * j4);
+                  cvt_fma2(yy[2 * j4], r[8 * c1 + 4 * j4], r[8 * c1 + 4 * j4 + 1], mul2_u(sx2, pack2(w4.x, w4.y)));
+                  cvt_fma2(yy[2 * j4 + 1], r[8 * c1 + 4 * j4 + 2], r[8 * c1 + 4 * j4 + 3],
+                           mul2_u(sx2, pack2(w4.z, w4.w)));
+                }
+              }
+            }
+          }
+        }
+        if (kAccOut) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(leader_tempty + acc * 8);
+        }
+        trace(tr_cta && threadIdx.x == 0, 3 + 2 * h, g);
+        if (h == 0) sx_next = fetch_sx(g + 1, b + 1 == nb ? 0 : b + 1);
+      }
+
+      if (++b == nb) {
+        // -------------------------------------------- a8: tile write-back ----
+        if (!kAccOut) {
+          int m0, n0;
+          sched.coords(t, m0, n0);
+          const int mw = m0 + 128 * (int)crank + 32 * q;  // first row of this warp's boxes
+          const uint32_t ybuf = opaque(sbase + C::kYBase + warp * 4 * C::kYBoxBytes);
+          if (lane == 0) bulk_wait_group_read0();  // previous tile's stores have left smem
+          __syncwarp();
+#pragma unroll
+          for (int bx = 0; bx < 4; ++bx) {  // box = (item h, unit u): 32 rows x 16 columns
+            const int h = bx >> 1, u = bx & 1;
+            const uint32_t swa = slot + C::kSwOff + pf_col(h, 32 * kw + 16 * u) * 4;
+            uint32_t hw[8];
+#pragma unroll
+            for (int p4 = 0; p4 < 4; ++p4) {
+              uint64_t v0 = y[16 * h + 8 * u + 2 * p4], v1 = y[16 * h + 8 * u + 2 * p4 + 1];
+              if (kGroupK) {  // per-channel weight scales, once per tile
+                const float4 w4 = lds_f32x4(swa + 16 * p4);
+                v0 = mul2_u(v0, pack2(w4.x, w4.y));
+                v1 = mul2_u(v1, pack2(w4.z, w4.w));
+              }
+              __half2 h0 = __float22half2_rn(unpack2(v0));
+              __half2 h1 = __float22half2_rn(unpack2(v1));
+              hw[2 * p4] = *reinterpret_cast<uint32_t*>(&h0);
+              hw[2 * p4 + 1] = *reinterpret_cast<uint32_t*>(&h1);
+              y[16 * h + 8 * u + 2 * p4] = 0;
+              y[16 * h + 8 * u + 2 * p4 + 1] = 0;
+            }
+            const uint32_t dst = ybuf + bx * C::kYBoxBytes + (opaque(threadIdx.x) & 31) * 32;
+            sts128(dst, make_uint4(hw[0], hw[1], hw[2], hw[3]));
+            sts128(dst + 16, make_uint4(hw[4], hw[5], hw[6], hw[7]));
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+#pragma unroll
+            for (int bx = 0; bx < 4; ++bx) {
+              const int nglob = n0 + pf_col(bx >> 1, 32 * kw + 16 * (bx & 1));
+              if (nglob < args.N) tma_store_2d(&tmY, ybuf + bx * C::kYBoxBytes, nglob, mw);
+            }
+            bulk_commit_group();
+          }
+        }
+        b = 0;
+        t += sched.clusters;
+      }
+      __syncwarp();
+      if (!kAccOut && lane == 0) mbar_arrive(&sempty[a]);
+    }
+  }
+
+  if (!kAccOut && warp < 12 && lane == 0) bulk_wait_group0();  // output stores complete
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == C::kMmaWarp) tmem_dealloc_2sm<512>(tmem_base);
+}
+
+}  // namespace comet

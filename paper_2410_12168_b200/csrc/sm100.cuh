@@ -81,6 +81,26 @@ DEVI bool mbar_test_cluster(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+// non-blocking probe at CTA scope, made warp-uniform (lane 0's answer)
+DEVI bool mbar_test_warp(const uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return __shfl_sync(0xffffffffu, ok, 0) != 0;
+}
+DEVI bool mbar_test_cluster_warp(const uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return __shfl_sync(0xffffffffu, ok, 0) != 0;
+}
+
 // ----------------------------------------------------------------- TMA ----
 // 2-D tiled store shared -> global (bulk async-group completion; OOB elements
 // of the box are not written)
@@ -180,6 +200,11 @@ DEVI void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "me
 DEVI void tmem_ld_32x32b_x8(uint32_t taddr, uint32_t (&r)[8]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+DEVI void tmem_ld_32x32b_x4(uint32_t taddr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                : "r"(taddr));
 }
 // wait::ld that also "redefines" the loaded registers, so no use of them can
@@ -352,6 +377,17 @@ DEVI void cvt_fma2_magic(uint64_t& y, uint32_t a0, uint32_t a1, uint64_t s) {
       : "+l"(y)
       : "r"(a0), "r"(a1), "l"(s), "l"(0xCB400000CB400000ull));
 }
+// Same result with the INT32 -> fp32 conversion on the FMA pipe (IMAD with a
+// multiplier the compiler cannot see is 1, then an exact FADD2): used for a
+// fraction of the columns to move work off the half-rate ALU pipe (I2F).
+DEVI void cvt_fma2_fmapipe(uint64_t& y, uint32_t a0, uint32_t a1, uint64_t s, uint32_t one) {
+  asm("{\n .reg .b32 lo, hi;\n .reg .b64 p;\n"
+      " mad.lo.u32 lo, %1, %4, 0x4B400000;\n mad.lo.u32 hi, %2, %4, 0x4B400000;\n mov.b64 p, {lo, hi};\n"
+      " add.rn.f32x2 p, p, %5;\n"
+      " fma.rn.f32x2 %0, p, %3, %0;\n}\n"
+      : "+l"(y)
+      : "r"(a0), "r"(a1), "l"(s), "r"(one), "l"(0xCB400000CB400000ull));
+}
 // 16 B of shared memory as two packed fp32 pairs
 DEVI void lds_u64x2(uint32_t addr, uint64_t& a, uint64_t& b) {
   asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(addr));
@@ -409,6 +445,13 @@ DEVI void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
       : "memory");
 }
 
+// 32 lanes x 8 columns from registers
+DEVI void tmem_st_32x32b_x8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+
 // 32 lanes x 16 columns, every column set to v
 DEVI void tmem_fill_32x32b_x16(uint32_t taddr, uint32_t v) {
   asm volatile(
@@ -429,5 +472,18 @@ DEVI void magic_fma2(uint64_t& y, uint32_t a0, uint32_t a1, uint64_t s) {
       : "+l"(y)
       : "r"(a0), "r"(a1), "l"(s), "l"(0xCB400000CB400000ull));
 }
+
+// an opaque copy: values derived from it are recomputed where used instead
+// of being hoisted out of loops (and spilled) by the compiler
+DEVI uint32_t opaque(uint32_t v) {
+  asm volatile("mov.b32 %0, %0;" : "+r"(v));
+  return v;
+}
+
+// per-warpgroup register budget (all 4 warps of the warpgroup execute it)
+template <int N>
+DEVI void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
+template <int N>
+DEVI void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
 
 }  // namespace comet

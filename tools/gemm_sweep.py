@@ -172,6 +172,26 @@ def trace(M, N, K, n8, cta=0, units=24):
         print(f"{i:4d} " + " ".join(f"{a[e, i] - t0:7d}" for e in range(10)))
 
 
+def trace3(M, N, K, n8, cta=0, steps=40):
+    """TMEM-A prefill kernel (gemm_pf.cuh): per-step event timeline of one CTA"""
+    import ctypes
+    L = comet.lib()
+    L.comet_debug_cta_times.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
+    L.comet_debug_trace.argtypes = [ctypes.c_void_p]
+    buf = (ctypes.c_ulonglong * 768)()
+    L.comet_debug_cta_times(cta + 1, None, 0)
+    run(M, N, K, n8, "K", reps=1)
+    L.comet_debug_cta_times(0, None, 0)
+    L.comet_debug_trace(buf)
+    a = np.array(buf[:], dtype=np.int64).reshape(12, 64)
+    t0 = a[0, 0]
+    names = ["Ptop", "staged", "tfull0", "prom0", "tfull1", "prom1", "ready", "mma0", "mma1", "Wiss", "Xiss", "sxrdy"]
+    print(f"M={M} N={N} K={K} CTA{cta} pf trace (cycles rel. first P iteration; staged = block g+2 staged):")
+    print("step " + " ".join(f"{n:>7s}" for n in names))
+    for i in range(steps):
+        print(f"{i:4d} " + " ".join(f"{a[e, i] - t0:7d}" for e in range(12)))
+
+
 def trace2(M, N, K, n8, cta=0, steps=40):
     """prefill (CTA-pair) kernel: per-step event timeline of one CTA's compute warp 0"""
     import ctypes
