@@ -54,9 +54,28 @@ DEVI void mma_i8_ts_2sm(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint3
 #endif
 constexpr bool kTraceEv2 = COMET_TRACE_EV2;
 
-#ifndef COMET_PF_FMAPIPE
-#define COMET_PF_FMAPIPE 0  // of every 4 column pairs, this many convert on the FMA pipe
+#ifndef COMET_PF_MAGIC
+#define COMET_PF_MAGIC 0  // 1: magic-biased accumulators (below; measured 1.6x slower: register spills + refill latency)
 #endif
+// Magic-biased accumulators (SURVEY 7.3-1 iii): the promotion warps refill
+// each accumulator with the bit pattern 0x4B400000 (= 1.5*2^23 as fp32) right
+// after reading it, and the MMAs accumulate onto it (enable_input_d = 1 from
+// the first K step), so the INT32 result a (|a| < 2^21 for both block kinds)
+// arrives as the fp32 value 1.5*2^23 + a: one exact FADD2 converts two
+// columns (vs two I2F on the half-rate ALU pipe) -- bit-identical results.
+constexpr bool kPfMagic = COMET_PF_MAGIC;
+
+#ifndef COMET_PF_SLEEP
+#define COMET_PF_SLEEP 7  // waits that suspend: 1 producer, 2 MMA issuer, 4 staging warps
+#endif
+template <int kSleep>
+DEVI void pf_wait(uint64_t* bar, uint32_t parity) {
+  if (kSleep) mbar_wait_sleep(bar, parity); else mbar_wait(bar, parity);
+}
+template <int kSleep>
+DEVI void pf_wait_cluster(uint64_t* bar, uint32_t parity) {
+  if (kSleep) mbar_wait_cluster_sleep(bar, parity); else mbar_wait_cluster(bar, parity);
+}
 
 struct PfCfg {
   static constexpr int kTileN = 192;          // weight rows per pair tile
@@ -180,9 +199,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
       const int s = g % C::kStages, x = g % C::kXStages;
       const int a = g & (C::kScaleSlots - 1);
       // weights: stage s is free once the MMAs of block g - kStages are done
-      mbar_wait(&wempty[s], ((g / C::kStages) & 1) ^ 1);
-      mbar_wait(&xempty[x], ((g / C::kXStages) & 1) ^ 1);
-      if (!kAccOut) mbar_wait(&sempty[a], ((g / C::kScaleSlots) & 1) ^ 1);
+      // (the producer, MMA and staging warps run ahead of the promotion: their
+      // waits suspend instead of polling, leaving issue slots to the promotion)
+      pf_wait<COMET_PF_SLEEP & 1>(&wempty[s], ((g / C::kStages) & 1) ^ 1);
+      pf_wait<COMET_PF_SLEEP & 1>(&xempty[x], ((g / C::kXStages) & 1) ^ 1);
+      if (!kAccOut) pf_wait<COMET_PF_SLEEP & 1>(&sempty[a], ((g / C::kScaleSlots) & 1) ^ 1);
       const uint32_t code = map.code[b];
       const bool is8 = (code >> 15) != 0;
       const int rank = code & 0x7FFF;
@@ -238,8 +259,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
     for (int i = 0; i < 2 * steps && crank == 0; ++i) {
       const int g = i >> 1, h = i & 1;
       const int s = g % C::kStages, acc = i % C::kAccs;
-      if (h == 0) mbar_wait_cluster(&ready[s], (g / C::kStages) & 1);
-      mbar_wait_cluster(&tempty[acc], ((i / C::kAccs) & 1) ^ 1);
+      if (h == 0) pf_wait_cluster<COMET_PF_SLEEP & 2>(&ready[s], (g / C::kStages) & 1);
+      // magic mode: use k of an accumulator waits for its k-th refill (the
+      // promotion warps' initial fill is completion 0)
+      pf_wait_cluster<COMET_PF_SLEEP & 2>(&tempty[acc], ((i / C::kAccs) & 1) ^ (kPfMagic ? 0 : 1));
       tc_fence_after();
       if (elect_one()) {
         const uint32_t a_tm = tmem_base + C::kAOff + 32 * s;
@@ -247,7 +270,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           mma_i8_ts_2sm(tmem_base + acc * C::kAccCols, a_tm + 8 * k,
-                        umma_desc_sw128_kmajor(bst + h * 48 * 128 + 32 * k), idesc, k > 0 ? 1u : 0u);
+                        umma_desc_sw128_kmajor(bst + h * 48 * 128 + 32 * k), idesc, (kPfMagic || k > 0) ? 1u : 0u);
         mma_commit_2sm(&tfull[acc], 0x3);
         if (h == 1) mma_commit_2sm(&wempty[s], 0x3);
         trace(tr_cta, 7 + h, g);
@@ -269,8 +292,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
       if (++sb == nb) sb = 0;
       const uint32_t xs = sbase + C::kXBase + x * C::kXStageBytes;
       const uint32_t wst = sbase + s * C::kWStageBytes;
-      mbar_wait(&xfull[x], (j / C::kXStages) & 1);
-      mbar_wait(&wfull[s], (j / C::kStages) & 1);
+      pf_wait<COMET_PF_SLEEP & 4>(&xfull[x], (j / C::kXStages) & 1);
+      pf_wait<COMET_PF_SLEEP & 4>(&wfull[s], (j / C::kStages) & 1);
       trace(tr_cta && threadIdx.x == 384, 10, j);
       tc_fence_after();
       // all shared-memory loads of the block first (the loads and stores are
@@ -354,7 +377,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
       return lds_f32(scale_base + a * C::kSlotBytes + row * 4) * (is8 ? 0.0625f : 0.00390625f);
     };
     float sx_next = fetch_sx(0, 0);
-    const uint32_t one = opaque(1u);
+    if (kPfMagic) {
+      // initial fill of this warp's 32 columns of every accumulator
+#pragma unroll
+      for (int acc = 0; acc < C::kAccs; ++acc) tmem_fill_32x32b_x32(tl + acc * C::kAccCols, kAccMagic);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0)
+        for (int acc = 0; acc < C::kAccs; ++acc) mbar_arrive_cluster(leader_tempty + acc * 8);
+    }
     for (int g = 0; g < steps; ++g) {
       trace(tr_cta && threadIdx.x == 0, 0, g);
       const int a = g & (C::kScaleSlots - 1);
@@ -381,11 +413,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
             uint32_t r[16];
             tmem_ld_32x32b_x16(ta + 16 * u, r);
             tmem_ld_wait();
+            if (kPfMagic && u == 1) tmem_fill_32x32b_x32(ta, kAccMagic);
             if (m < args.M) {
               const int nu = n0 + pf_col(h, 32 * kw + 16 * u);
 #pragma unroll
               for (int j = 0; j < 16; ++j)
-                if (nu + j < args.N) args.Acc[((int64_t)b * args.M + m) * args.N + nu + j] = ((int32_t)r[j]) >> sh;
+                if (nu + j < args.N)
+                  args.Acc[((int64_t)b * args.M + m) * args.N + nu + j] =
+                      ((int32_t)(r[j] - (kPfMagic ? kAccMagic : 0u))) >> sh;
             }
           }
         } else {
@@ -397,6 +432,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
             tmem_ld_32x32b_x16(ta + 16 * c2, r);
             tmem_ld_wait();
             if (c2 == 1) {
+              if (kPfMagic) {
+                tmem_fill_32x32b_x32(ta, kAccMagic);
+                tmem_st_wait();
+              }
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive_cluster(leader_tempty + acc * 8);
@@ -408,8 +447,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
               if (kGroupK) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                  if (j < COMET_PF_FMAPIPE)  // exact: |acc'| < 2^22 (SURVEY 7.3-1 iii)
-                    cvt_fma2_fmapipe(yy[j], r[8 * c1 + 2 * j], r[8 * c1 + 2 * j + 1], sx2, one);
+                  if (kPfMagic)
+                    magic_fma2(yy[j], r[8 * c1 + 2 * j], r[8 * c1 + 2 * j + 1], sx2);
                   else
                     cvt_fma2(yy[j], r[8 * c1 + 2 * j], r[8 * c1 + 2 * j + 1], sx2);
                 }
@@ -419,15 +458,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
 #pragma unroll
                 for (int j4 = 0; j4 < 2; ++j4) {
                   const float4 w4 = lds_f32x4(swa + 16 * j4);
-                  cvt_fma2(yy[2 * j4], r[8 * c1 + 4 * j4], r[8 * c1 + 4 * j4 + 1], mul2_u(sx2, pack2(w4.x, w4.y)));
-                  cvt_fma2(yy[2 * j4 + 1], r[8 * c1 + 4 * j4 + 2], r[8 * c1 + 4 * j4 + 3],
-                           mul2_u(sx2, pack2(w4.z, w4.w)));
+                  const uint64_t s01 = mul2_u(sx2, pack2(w4.x, w4.y)), s23 = mul2_u(sx2, pack2(w4.z, w4.w));
+                  if (kPfMagic) {
+                    magic_fma2(yy[2 * j4], r[8 * c1 + 4 * j4], r[8 * c1 + 4 * j4 + 1], s01);
+                    magic_fma2(yy[2 * j4 + 1], r[8 * c1 + 4 * j4 + 2], r[8 * c1 + 4 * j4 + 3], s23);
+                  } else {
+                    cvt_fma2(yy[2 * j4], r[8 * c1 + 4 * j4], r[8 * c1 + 4 * j4 + 1], s01);
+                    cvt_fma2(yy[2 * j4 + 1], r[8 * c1 + 4 * j4 + 2], r[8 * c1 + 4 * j4 + 3], s23);
+                  }
                 }
               }
             }
           }
         }
         if (kAccOut) {
+          if (kPfMagic) tmem_st_wait();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(leader_tempty + acc * 8);

@@ -270,6 +270,19 @@ DEVI void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait_cluster(bar, parity)) {
   }
 }
+DEVI bool mbar_try_wait_cluster_suspend(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(kMbarSuspendNs)
+      : "memory");
+  return ok != 0;
+}
+DEVI void mbar_wait_cluster_sleep(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait_cluster_suspend(bar, parity)) {
+  }
+}
 DEVI void fence_acq_rel_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
 
 template <uint32_t kCols>
@@ -456,6 +469,15 @@ DEVI void tmem_st_32x32b_x8(uint32_t taddr, const uint32_t (&r)[8]) {
 DEVI void tmem_fill_32x32b_x16(uint32_t taddr, uint32_t v) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(v)
+      : "memory");
+}
+
+// 32 lanes x 32 columns, every column set to v
+DEVI void tmem_fill_32x32b_x32(uint32_t taddr, uint32_t v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+      "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
       "r"(v)
       : "memory");
 }
