@@ -66,7 +66,7 @@ constexpr bool kTraceEv2 = COMET_TRACE_EV2;
 constexpr bool kPfMagic = COMET_PF_MAGIC;
 
 #ifndef COMET_PF_SLEEP
-#define COMET_PF_SLEEP 7  // waits that suspend: 1 producer, 2 MMA issuer, 4 staging warps
+#define COMET_PF_SLEEP 0  // waits that suspend: 1 producer, 2 MMA issuer, 4 staging warps
 #endif
 template <int kSleep>
 DEVI void pf_wait(uint64_t* bar, uint32_t parity) {
@@ -85,13 +85,19 @@ struct PfCfg {
   static constexpr int kTileN = 192;          // weight rows per pair tile
   static constexpr int kRows = kTileN / 2;    // weight rows per CTA
 #ifndef COMET_PF_ITEMS
-#define COMET_PF_ITEMS 2
+#define COMET_PF_ITEMS 1
 #endif
   static constexpr int kItems = COMET_PF_ITEMS;  // MMA items per block (1: N=192; 2: N=96 halves)
   static constexpr int kItemN = kTileN / kItems;  // MMA N of one item (kItemN/2 rows from each CTA)
   static constexpr int kWCols = kItemN / 3;       // item columns per promotion warp (3 per lane quarter)
-  static constexpr int kStages = 4;           // operand stages: SW128 B operand + TMEM A slot (freed by the MMA)
-  static constexpr int kLStages = 4;          // load stages: packed weights + raw tokens (freed by the staging warps)
+#ifndef COMET_PF_LSTAGES
+#define COMET_PF_LSTAGES 5
+#endif
+#ifndef COMET_PF_STAGES
+#define COMET_PF_STAGES 4
+#endif
+  static constexpr int kStages = COMET_PF_STAGES;    // operand stages: SW128 B + TMEM A slot (freed by the MMA)
+  static constexpr int kLStages = COMET_PF_LSTAGES;  // load stages: packed weights + raw tokens (freed by staging)
   static constexpr int kAccs = kItems == 1 ? 2 : 4;  // kItemN-column accumulators
   static constexpr int kScaleSlots = 8;
   static constexpr int kWPBytes = kRows * 64;   // packed weights
@@ -113,9 +119,10 @@ struct PfCfg {
   static constexpr int kAccCols = kItemN;
   static constexpr int kAOff = kAccs * kAccCols;  // TMEM A slots after the accumulators
   static_assert(kAOff + 32 * kStages <= 512, "TMEM budget");
-  static constexpr int kThreads = 576;
-  static constexpr int kLoadWarp = 16;
+  static constexpr int kThreads = 640;
+  static constexpr int kLoadWarp = 16;   // weights
   static constexpr int kMmaWarp = 17;
+  static constexpr int kLoad2Warp = 18;  // tokens + scales (warp 19 idle)
   static constexpr int kReadyCount = 2 * 4;         // both CTAs' staging warps
   static constexpr int kTemptyCount = 2 * 12;       // both CTAs' promotion warps
 };
@@ -138,7 +145,7 @@ __host__ __device__ constexpr int pf_col(int h, int j) {
 }
 
 template <bool kGroupK, bool kAccOut>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
     w4ax_gemm_pf_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmX4,
                         const __grid_constant__ CUtensorMap tmX8, const __grid_constant__ BlockMap map, GemmArgs args,
                         PfSched sched) {
@@ -175,7 +182,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
       mbar_init(&ready[s], C::kReadyCount);
     }
     for (int l = 0; l < C::kLStages; ++l) {
-      mbar_init(&lfull[l], 1);
+      mbar_init(&lfull[l], 2);  // two producers
       mbar_init(&lempty[l], 4);
     }
     for (int a = 0; a < C::kAccs; ++a) {
@@ -201,8 +208,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
   // debug trace of one CTA (COMET_TRACE builds; tools/gemm_sweep.py trace3)
   const bool tr_cta = kTraceBuild && g_cta_times_on && blockIdx.x + 1 == g_cta_times_on;
 
-  if (warp == C::kLoadWarp) {
-    // ------------------------------------------------- a3: producer ----
+  if (warp == C::kLoadWarp || warp == C::kLoad2Warp) {
+    // ------------------- a3: producers (weights | tokens + scales) ----
+    // two warps: each TMA / bulk-copy issue costs the issuing thread ~10^2
+    // cycles, and one thread issuing all of a block's copies was the rate limit
+    const bool wrole = warp == C::kLoadWarp;
     int pg = 0, pt = cluster, pb = 0, pm0 = 0, pn0 = 0;
     sched.coords(pt, pm0, pn0);
     for (; pg < steps;) {
@@ -215,42 +225,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
       // (the producer, MMA and staging warps run ahead of the promotion: their
       // waits suspend instead of polling, leaving issue slots to the promotion)
       pf_wait<COMET_PF_SLEEP & 1>(&lempty[l], ((g / C::kLStages) & 1) ^ 1);
-      if (!kAccOut) pf_wait<COMET_PF_SLEEP & 1>(&sempty[a], ((g / C::kScaleSlots) & 1) ^ 1);
+      if (!kAccOut && !wrole) pf_wait<COMET_PF_SLEEP & 1>(&sempty[a], ((g / C::kScaleSlots) & 1) ^ 1);
       const uint32_t code = map.code[b];
       const bool is8 = (code >> 15) != 0;
       const int rank = code & 0x7FFF;
       const int my_m0 = pm0 + 128 * (int)crank;
       if (elect_one()) {
-        // this CTA's weight rows [R, R + v) of the tile (v < 96 at the right
-        // edge of N); in the tiled layout they are contiguous within each
-        // 128-row slab
-        const int R = pn0 + C::kRows * (int)crank;
-        const int v = max(0, min(C::kRows, args.N - R));
-        mbar_arrive_expect_tx(&lfull[l], COMET_PF_EXP >= 5 ? 0 : v * 64 + (is8 ? 128 * 128 : 128 * 64));
-        uint8_t* dst = smem + C::kWPBase + l * C::kWPBytes;
-        int r = R, left = COMET_PF_EXP >= 5 ? 0 : v;
-        while (left > 0) {
-          const int in_slab = min(left, 128 - (r & 127));
-          bulk_load(dst, args.Wq + ((int64_t)(r >> 7) * nb + b) * 8192 + (r & 127) * 64, in_slab * 64, &lfull[l]);
-          dst += in_slab * 64;
-          r += in_slab;
-          left -= in_slab;
-        }
-        uint8_t* xs = smem + C::kXBase + l * C::kXStageBytes;
-        if (COMET_PF_EXP >= 5) {
-        } else if (is8)
-          tma_load_2d(xs, &tmX8, &lfull[l], rank * 128, my_m0);
-        else
-          tma_load_2d(xs, &tmX4, &lfull[l], rank * 64, my_m0);
-        if (!kAccOut) {
-          const int nsx = max(0, min(128, (int)args.ldsx - my_m0));  // multiple of 4
-          const bool load_sw = !kGroupK || b == nb - 1;
-          const int nsw = load_sw ? max(0, min(C::kTileN, args.N - pn0)) : 0;  // multiple of 64
-          mbar_arrive_expect_tx(&sfull[a], (nsx + nsw) * 4);
-          uint8_t* slot = smem + C::kScaleBase + a * C::kSlotBytes;
-          if (nsx) bulk_load(slot, args.Sx + (int64_t)b * args.ldsx + my_m0, nsx * 4, &sfull[a]);
-          if (nsw)
-            bulk_load(slot + C::kSwOff, args.Sw + (kGroupK ? 0 : (int64_t)b * args.N) + pn0, nsw * 4, &sfull[a]);
+        if (wrole) {
+          // this CTA's weight rows [R, R + v) of the tile (v < 96 at the right
+          // edge of N); in the tiled layout they are contiguous within each
+          // 128-row slab
+          const int R = pn0 + C::kRows * (int)crank;
+          const int v = max(0, min(C::kRows, args.N - R));
+          mbar_arrive_expect_tx(&lfull[l], COMET_PF_EXP == 5 ? 0 : v * 64);
+          uint8_t* dst = smem + C::kWPBase + l * C::kWPBytes;
+          int r = R, left = COMET_PF_EXP == 5 ? 0 : v;
+          while (left > 0) {
+            const int in_slab = min(left, 128 - (r & 127));
+            bulk_load(dst, args.Wq + ((int64_t)(r >> 7) * nb + b) * 8192 + (r & 127) * 64, in_slab * 64, &lfull[l]);
+            dst += in_slab * 64;
+            r += in_slab;
+            left -= in_slab;
+          }
+        } else {
+          mbar_arrive_expect_tx(&lfull[l], COMET_PF_EXP >= 5 ? 0 : (is8 ? 128 * 128 : 128 * 64));
+          uint8_t* xs = smem + C::kXBase + l * C::kXStageBytes;
+          if (COMET_PF_EXP >= 5) {  // 5: no operand loads, 6: no token loads
+          } else if (is8)
+            tma_load_2d(xs, &tmX8, &lfull[l], rank * 128, my_m0);
+          else
+            tma_load_2d(xs, &tmX4, &lfull[l], rank * 64, my_m0);
+          if (!kAccOut) {
+            const int nsx = max(0, min(128, (int)args.ldsx - my_m0));  // multiple of 4
+            const bool load_sw = !kGroupK || b == nb - 1;
+            const int nsw = load_sw ? max(0, min(C::kTileN, args.N - pn0)) : 0;  // multiple of 64
+            mbar_arrive_expect_tx(&sfull[a], (nsx + nsw) * 4);
+            uint8_t* slot = smem + C::kScaleBase + a * C::kSlotBytes;
+            if (nsx) bulk_load(slot, args.Sx + (int64_t)b * args.ldsx + my_m0, nsx * 4, &sfull[a]);
+            if (nsw)
+              bulk_load(slot + C::kSwOff, args.Sw + (kGroupK ? 0 : (int64_t)b * args.N) + pn0, nsw * 4, &sfull[a]);
+          }
         }
         trace(!kTraceEv2 && tr_cta, 9, g);
       }
@@ -290,7 +304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
       }
       __syncwarp();
     }
-  } else if (warp >= 12) {
+  } else if (warp >= 12 && warp < 16) {
     // ---- warps 12-15: a4 staging (thread = token row of lane quarter q) ----
     const int q = warp & 3;
     const int et = threadIdx.x - 384;  // 0..127
@@ -372,7 +386,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
       if (lane == 0) mbar_arrive_cluster(leader_ready + s * 8);
       trace(tr_cta && threadIdx.x == 384, 1, j);
     }
-  } else {
+  } else if (warp < 12) {
     // ------------------------ warps 0-11: a6 promotion + a8 write-back ----
     const int q = warp & 3;         // TMEM lane quarter
     const int kw = warp >> 2;       // 0..2: item columns [kWCols kw, kWCols (kw + 1)) of every item
