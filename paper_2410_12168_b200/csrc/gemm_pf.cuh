@@ -81,6 +81,10 @@ DEVI void pf_wait_cluster(uint64_t* bar, uint32_t parity) {
 #define COMET_PF_EXP 0  // timing experiments only (wrong results): 1 = skip staging work, 2 = skip promotion math, 3 = both, 4 = also skip the accumulator loads, 5 = also skip the operand loads
 #endif
 
+#ifndef COMET_PF_LDPIPE
+#define COMET_PF_LDPIPE 1  // double-buffered 8-column accumulator loads in the promotion
+#endif
+
 struct PfCfg {
   static constexpr int kTileN = 192;          // weight rows per pair tile
   static constexpr int kRows = kTileN / 2;    // weight rows per CTA
@@ -454,6 +458,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
                   args.Acc[((int64_t)b * args.M + m) * args.N + nu + j] =
                       ((int32_t)(r[j] - (kPfMagic ? kAccMagic : 0u))) >> sh;
             }
+          }
+        } else if (COMET_PF_LDPIPE && !kPfMagic && COMET_PF_EXP == 0) {
+          // 8-column chunks, double-buffered: the load of chunk c + 1 is in
+          // flight while chunk c is promoted, so the accumulator's hold time
+          // is the load stream, not loads + math; released after the last load
+          auto promote8 = [&](int c, const uint32_t (&r)[8]) {
+            uint64_t* yy = &y[(kWC / 2) * h + 4 * c];
+            if (kGroupK) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) cvt_fma2(yy[j], r[2 * j], r[2 * j + 1], sx2);
+            } else {
+              const uint32_t swa = slot + C::kSwOff + pf_col(h, kWC * kw + 8 * c) * 4;
+#pragma unroll
+              for (int j4 = 0; j4 < 2; ++j4) {
+                const float4 w4 = lds_f32x4(swa + 16 * j4);
+                cvt_fma2(yy[2 * j4], r[4 * j4], r[4 * j4 + 1], mul2_u(sx2, pack2(w4.x, w4.y)));
+                cvt_fma2(yy[2 * j4 + 1], r[4 * j4 + 2], r[4 * j4 + 3], mul2_u(sx2, pack2(w4.z, w4.w)));
+              }
+            }
+          };
+          constexpr int kC = kWC / 8;
+          uint32_t ra[8], rb[8];
+          tmem_ld_32x32b_x8(ta, ra);
+          tmem_ld_wait_dep(ra);
+#pragma unroll
+          for (int c = 0; c < kC; c += 2) {
+            tmem_ld_32x32b_x8(ta + 8 * (c + 1), rb);
+            promote8(c, ra);
+            tmem_ld_wait_dep(rb);
+            if (c + 2 < kC) {
+              tmem_ld_32x32b_x8(ta + 8 * (c + 2), ra);
+            } else {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive_cluster(leader_tempty + acc * 8);
+            }
+            promote8(c + 1, rb);
+            if (c + 2 < kC) tmem_ld_wait_dep(ra);
           }
         } else {
           // 16 columns per tcgen05.ld (the running sums leave room for 16);
