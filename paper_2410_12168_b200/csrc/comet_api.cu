@@ -413,9 +413,7 @@ comet_status comet_pack_weight(const void* W, int64_t ldw, int32_t N, int32_t K,
     // group-128 weights are "activations" with an all-INT4 mask, Sw = Sx with ldsx = N
     BlockMap map;
     for (int b = 0; b < 512; ++b) map.code[b] = (uint16_t)(b < K / 128 ? b : 0);
-    const int64_t items = ((int64_t)N + 7) / 8 * 8 * (K / 128);
-    int grid = (int)((items + 15) / 16);
-    if (grid > 148 * 16) grid = 148 * 16;
+    const dim3 grid((unsigned)((N + 7) / 8), (unsigned)((K / 128 + 1) / 2));
     // Sw layout [K/128 x N] is the Sx layout with ldsx == N (no padding rows)
     if (perm)
       quantize_act_kernel<true, true><<<grid, 256, 0, st>>>(Wh, ldw, N, K / 128, N, perm, map, nullptr, 0,
@@ -450,15 +448,39 @@ comet_status comet_quantize_act(const void* X, int64_t ldx, int32_t M, int32_t K
   comet_status ds = device_check(&num_sms);
   if (ds != COMET_OK) return ds;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int64_t items = (ldsx + 7) / 8 * 8 * (K / 128);
-  int64_t grid = (items + 15) / 16;
-  if (grid > (int64_t)num_sms * 16) grid = (int64_t)num_sms * 16;
   const __half* Xh = reinterpret_cast<const __half*>(X);
+  if (M >= 64) {
+    // row-staged kernel: persistent CTAs, double-buffered rows in smem
+    const int smem = 2 * K * 2 + ((perm && COMET_Q_PERMSMEM) ? K * 2 : 0);  // two row buffers + u16 permutation
+    if (smem <= 200 * 1024) {
+      // (dynamic smem above the 48 KB default needs the opt-in; set per call,
+      // it is a cheap host-side attribute)
+      cudaError_t e = cudaFuncSetAttribute(perm ? quantize_act_rows_kernel<true> : quantize_act_rows_kernel<false>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return cuda_fail(e);
+      int per_sm = (228 * 1024) / (smem + 1024);
+      if (per_sm > 8) per_sm = 8;
+      if (per_sm < 1) per_sm = 1;
+      int64_t grid = (int64_t)num_sms * per_sm;
+      if (grid > ldsx) grid = ldsx;
+      if (perm)
+        quantize_act_rows_kernel<true><<<(int)grid, 256, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8,
+                                                                      (int64_t)n8 * 128, reinterpret_cast<uint8_t*>(Xq4),
+                                                                      (int64_t)n4 * 64, Sx);
+      else
+        quantize_act_rows_kernel<false><<<(int)grid, 256, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8,
+                                                                       (int64_t)n8 * 128, reinterpret_cast<uint8_t*>(Xq4),
+                                                                       (int64_t)n4 * 64, Sx);
+      return check_launch();
+    }
+  }
+  // one CTA per (8 rows, 2 blocks): 16 half-warp items
+  const dim3 grid((unsigned)((ldsx + 7) / 8), (unsigned)((K / 128 + 1) / 2));
   if (perm)
-    quantize_act_kernel<true><<<(int)grid, 256, 0, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
+    quantize_act_kernel<true><<<grid, 256, 0, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
                                                           reinterpret_cast<uint8_t*>(Xq4), (int64_t)n4 * 64, Sx);
   else
-    quantize_act_kernel<false><<<(int)grid, 256, 0, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
+    quantize_act_kernel<false><<<grid, 256, 0, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
                                                            reinterpret_cast<uint8_t*>(Xq4), (int64_t)n4 * 64, Sx);
   return check_launch();
 }

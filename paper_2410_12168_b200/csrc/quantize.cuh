@@ -79,6 +79,10 @@ DEVI int64_t wq_tiled_offset(int64_t n, int64_t p, int nb) {
 // Activation quantize + pack.  rows = ldsx (rows >= M get only Sx = 1.0).
 // kTiledW: the INT4 plane is a weight matrix written in the tiled layout
 // (comet_pack_weight, group 128).
+// Grid: blockIdx.x = group of 8 rows, blockIdx.y = pair of 128-channel
+// blocks; half-warp h of the CTA takes row 8x + (h & 7) of block 2y + (h >> 3)
+// (no 64-bit index arithmetic: the previous grid-stride form spent more
+// instructions on 64-bit item division than on the quantization).
 template <bool kPerm, bool kTiledW = false>
 __global__ void __launch_bounds__(256) quantize_act_kernel(const __half* __restrict__ X, int64_t ldx, int M, int nb,
                                                            int64_t ldsx, const int32_t* __restrict__ perm,
@@ -88,48 +92,170 @@ __global__ void __launch_bounds__(256) quantize_act_kernel(const __half* __restr
   const int half_id = threadIdx.x >> 4;  // 16 half-warps per CTA
   const int o = threadIdx.x & 15;        // octet within the block
   const unsigned hmask = 0xFFFFu << (threadIdx.x & 16);  // this half-warp's lanes
-  const int64_t n_groups = (ldsx + 7) / 8;
-  const int64_t items = n_groups * 8 * nb;
-  for (int64_t it = (int64_t)blockIdx.x * 16 + half_id; it < items; it += (int64_t)gridDim.x * 16) {
-    const int64_t g = it / (8 * nb);
-    const int rem = (int)(it - g * 8 * nb);
-    const int b = rem >> 3;
-    const int64_t m = g * 8 + (rem & 7);
-    if (m >= ldsx) continue;
-    if (m >= M) {
-      if (o == 0) Sx[(int64_t)b * ldsx + m] = 1.0f;
+  const int64_t m = (int64_t)blockIdx.x * 8 + (half_id & 7);
+  const int b = blockIdx.y * 2 + (half_id >> 3);
+  if (m >= ldsx || b >= nb) return;  // whole half-warps
+  if (m >= M) {
+    if (o == 0) Sx[(int64_t)b * ldsx + m] = 1.0f;
+    return;
+  }
+  float x[8];
+  load_octet<kPerm>(X, ldx, m, b, o, perm, x);
+  float a = 0.0f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a = fmaxf(a, fabsf(x[j]));
+#pragma unroll
+  for (int off = 8; off >= 1; off >>= 1) a = fmaxf(a, __shfl_xor_sync(hmask, a, off));
+  const uint32_t code = map.code[b];
+  const bool is8 = (code >> 15) != 0;
+  const int rank = code & 0x7FFF;
+  const float qmax = is8 ? 127.0f : 7.0f;
+  float s = 1.0f, r = 0.0f;
+  if (a != 0.0f) {
+    s = __fdiv_rn(a, qmax);
+    r = __fdiv_rn(qmax, a);
+  }
+  int32_t q[8];
+  quant8(x, r, q);
+  if (is8) {
+    uint32_t lo = (uint32_t)(q[0] & 0xFF) | ((uint32_t)(q[1] & 0xFF) << 8) | ((uint32_t)(q[2] & 0xFF) << 16) |
+                  ((uint32_t)(q[3] & 0xFF) << 24);
+    uint32_t hi = (uint32_t)(q[4] & 0xFF) | ((uint32_t)(q[5] & 0xFF) << 8) | ((uint32_t)(q[6] & 0xFF) << 16) |
+                  ((uint32_t)(q[7] & 0xFF) << 24);
+    *reinterpret_cast<uint2*>(Xq8 + m * ld8 + (int64_t)rank * 128 + o * 8) = make_uint2(lo, hi);
+  } else if (kTiledW) {
+    *reinterpret_cast<uint32_t*>(Xq4 + wq_tiled_offset(m, (int64_t)rank * 64 + o * 4, nb)) = pack_int4_word(q);
+  } else {
+    *reinterpret_cast<uint32_t*>(Xq4 + m * ld4 + (int64_t)rank * 64 + o * 4) = pack_int4_word(q);
+  }
+  if (o == 0) Sx[(int64_t)b * ldsx + m] = s;
+}
+
+// Activation quantize + pack, row-staged variant (a1 + a2 for the GEMM
+// path): persistent CTAs walk rows; each row (K fp16, contiguous) arrives in
+// shared memory by one 1-D bulk copy (the next row's copy is in flight while
+// this one is quantized), and the fused channel gather reads the
+// permuted positions from shared memory instead of issuing 8 scattered 2-byte
+// global loads per lane.  Half-warp per (row, 128-channel block) item, lane =
+// 8 channels, as in quantize_act_kernel (identical arithmetic and output).
+#ifndef COMET_Q_PERMSMEM
+#define COMET_Q_PERMSMEM 0  // 1: permutation cached in shared memory as u16 (measured slower: occupancy)
+#endif
+// One (row, block) item for the row-staged kernel: `row` is the row in
+// shared memory, `psm` the permutation as u16 in shared memory (kPerm).
+template <bool kPerm>
+DEVI void quant_item(const unsigned short* row, const unsigned short* psm, const int32_t* __restrict__ gperm,
+                     const BlockMap& map, int b, int o,
+                     unsigned hmask, int64_t m, int64_t ldsx, int8_t* __restrict__ Xq8, int64_t ld8,
+                     uint8_t* __restrict__ Xq4, int64_t ld4, float* __restrict__ Sx) {
+  const int i0 = b * 128 + o * 8;
+  float x[8];
+  if (kPerm && !COMET_Q_PERMSMEM) {
+    const int4 p0 = __ldg(reinterpret_cast<const int4*>(gperm + i0));
+    const int4 p1 = __ldg(reinterpret_cast<const int4*>(gperm + i0 + 4));
+    const int p[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = half_bits_to_float(row[p[j]]);
+  } else if (kPerm) {
+    const uint4 pv = *reinterpret_cast<const uint4*>(psm + i0);  // 8 x u16 source positions
+    const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      x[2 * j] = half_bits_to_float(row[pw[j] & 0xFFFF]);
+      x[2 * j + 1] = half_bits_to_float(row[pw[j] >> 16]);
+    }
+  } else {
+    const uint4 v = *reinterpret_cast<const uint4*>(row + i0);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      x[2 * j] = half_bits_to_float(w[j] & 0xFFFF);
+      x[2 * j + 1] = half_bits_to_float(w[j] >> 16);
+    }
+  }
+  float a = 0.0f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a = fmaxf(a, fabsf(x[j]));
+#pragma unroll
+  for (int off = 8; off >= 1; off >>= 1) a = fmaxf(a, __shfl_xor_sync(hmask, a, off));
+  const uint32_t code = map.code[b];
+  const bool is8 = (code >> 15) != 0;
+  const int rank = code & 0x7FFF;
+  const float qmax = is8 ? 127.0f : 7.0f;
+  float s = 1.0f, r = 0.0f;
+  if (a != 0.0f) {
+    s = __fdiv_rn(a, qmax);
+    r = __fdiv_rn(qmax, a);
+  }
+  int32_t q[8];
+  quant8(x, r, q);
+  if (is8) {
+    uint32_t lo = (uint32_t)(q[0] & 0xFF) | ((uint32_t)(q[1] & 0xFF) << 8) | ((uint32_t)(q[2] & 0xFF) << 16) |
+                  ((uint32_t)(q[3] & 0xFF) << 24);
+    uint32_t hi = (uint32_t)(q[4] & 0xFF) | ((uint32_t)(q[5] & 0xFF) << 8) | ((uint32_t)(q[6] & 0xFF) << 16) |
+                  ((uint32_t)(q[7] & 0xFF) << 24);
+    *reinterpret_cast<uint2*>(Xq8 + m * ld8 + (int64_t)rank * 128 + o * 8) = make_uint2(lo, hi);
+  } else {
+    *reinterpret_cast<uint32_t*>(Xq4 + m * ld4 + (int64_t)rank * 64 + o * 4) = pack_int4_word(q);
+  }
+  if (o == 0) Sx[(int64_t)b * ldsx + m] = s;
+}
+
+// Activation quantize + pack, row-staged variant (a1 + a2 for the GEMM
+// path): persistent CTAs walk rows; each row (K fp16, contiguous) arrives in
+// shared memory by one 1-D bulk copy (the next row's copy is in flight while
+// this one is quantized), the permutation sits in shared memory as u16 for
+// the CTA's lifetime, and the fused channel gather reads the
+// permuted positions from shared memory instead of issuing 8 scattered 2-byte
+// global loads per lane.  Half-warp per (row, 128-channel block) item, lane =
+// 8 channels, two items in flight per half-warp; arithmetic and output
+// identical to quantize_act_kernel.
+template <bool kPerm>
+__global__ void __launch_bounds__(256) quantize_act_rows_kernel(const __half* __restrict__ X, int64_t ldx, int M,
+                                                                int nb, int64_t ldsx, const int32_t* __restrict__ perm,
+                                                                const __grid_constant__ BlockMap map,
+                                                                int8_t* __restrict__ Xq8, int64_t ld8,
+                                                                uint8_t* __restrict__ Xq4, int64_t ld4,
+                                                                float* __restrict__ Sx) {
+  extern __shared__ __align__(16) uint8_t qsm[];
+  const int K = nb * 128;
+  __shared__ uint64_t rbar[2];
+  const int half_id = threadIdx.x >> 4;
+  const int o = threadIdx.x & 15;
+  const unsigned hmask = 0xFFFFu << (threadIdx.x & 16);
+  unsigned short* psm = reinterpret_cast<unsigned short*>(qsm + (size_t)4 * K);
+  if (threadIdx.x == 0) {
+    mbar_init(&rbar[0], 1);
+    mbar_init(&rbar[1], 1);
+    fence_mbar_init();
+  }
+  if (kPerm && COMET_Q_PERMSMEM)
+    for (int i = threadIdx.x; i < K; i += blockDim.x) psm[i] = (unsigned short)__ldg(perm + i);
+  __syncthreads();
+  auto issue = [&](int64_t m, int buf) {
+    mbar_arrive_expect_tx(&rbar[buf], (uint32_t)K * 2);
+    bulk_load(qsm + (size_t)buf * K * 2, X + m * ldx, (uint32_t)K * 2, &rbar[buf]);
+  };
+  int64_t m = blockIdx.x;
+  if (threadIdx.x == 0 && m < M) issue(m, 0);
+  for (int it = 0; m < ldsx; ++it, m += gridDim.x) {
+    const int buf = it & 1;
+    if (m >= M) {  // padding rows of the scale layout
+      for (int b = threadIdx.x; b < nb; b += blockDim.x) Sx[(int64_t)b * ldsx + m] = 1.0f;
       continue;
     }
-    float x[8];
-    load_octet<kPerm>(X, ldx, m, b, o, perm, x);
-    float a = 0.0f;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) a = fmaxf(a, fabsf(x[j]));
-#pragma unroll
-    for (int off = 8; off >= 1; off >>= 1) a = fmaxf(a, __shfl_xor_sync(hmask, a, off));
-    const uint32_t code = map.code[b];
-    const bool is8 = (code >> 15) != 0;
-    const int rank = code & 0x7FFF;
-    const float qmax = is8 ? 127.0f : 7.0f;
-    float s = 1.0f, r = 0.0f;
-    if (a != 0.0f) {
-      s = __fdiv_rn(a, qmax);
-      r = __fdiv_rn(qmax, a);
+    // prefetch the next row into the other buffer (its previous contents
+    // were consumed before the __syncthreads that ended the last iteration)
+    if (threadIdx.x == 0 && m + gridDim.x < M) issue(m + gridDim.x, buf ^ 1);
+    mbar_wait(&rbar[buf], (it >> 1) & 1);
+    const unsigned short* row = reinterpret_cast<const unsigned short*>(qsm + (size_t)buf * K * 2);
+    int b = half_id;
+    for (; b + 16 < nb; b += 32) {
+      quant_item<kPerm>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx);
+      quant_item<kPerm>(row, psm, perm, map, b + 16, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx);
     }
-    int32_t q[8];
-    quant8(x, r, q);
-    if (is8) {
-      uint32_t lo = (uint32_t)(q[0] & 0xFF) | ((uint32_t)(q[1] & 0xFF) << 8) | ((uint32_t)(q[2] & 0xFF) << 16) |
-                    ((uint32_t)(q[3] & 0xFF) << 24);
-      uint32_t hi = (uint32_t)(q[4] & 0xFF) | ((uint32_t)(q[5] & 0xFF) << 8) | ((uint32_t)(q[6] & 0xFF) << 16) |
-                    ((uint32_t)(q[7] & 0xFF) << 24);
-      *reinterpret_cast<uint2*>(Xq8 + m * ld8 + (int64_t)rank * 128 + o * 8) = make_uint2(lo, hi);
-    } else if (kTiledW) {
-      *reinterpret_cast<uint32_t*>(Xq4 + wq_tiled_offset(m, (int64_t)rank * 64 + o * 4, nb)) = pack_int4_word(q);
-    } else {
-      *reinterpret_cast<uint32_t*>(Xq4 + m * ld4 + (int64_t)rank * 64 + o * 4) = pack_int4_word(q);
-    }
-    if (o == 0) Sx[(int64_t)b * ldsx + m] = s;
+    if (b < nb) quant_item<kPerm>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx);
+    __syncthreads();  // every half-warp is done with this buffer
   }
 }
 
