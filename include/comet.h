@@ -138,6 +138,43 @@ comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K,
                                const uint8_t* block_bits, const void* Wq, const float* Sw, int32_t N, int32_t group,
                                void* Y, int64_t ldy, void* scratch, size_t scratch_bytes, comet_stream_t stream);
 
+/* ---- f2: FMPQ calibration (§3.2: outlier channels are identified
+ * "through data sampling", then clustered by a permutation) ---------------
+ * comet_calib_absmax: maxabs[c] = max(maxabs[c], max_m |X[m, c]|) over the
+ * calibration rows X fp16 [M x K] (DEVICE; row stride ldx, ldx % 8 == 0,
+ * K % 8 == 0); maxabs is a DEVICE fp32[K] the caller zero-initialises once
+ * and may accumulate over several batches (exact, order-independent).
+ * comet_fmpq_map (HOST, pure): from per-channel scores (maxabs, HOST fp32[K],
+ * K % 128 == 0) and theta > 1: median = lower middle of the sorted scores;
+ * channel c is an outlier iff score[c] > theta * median; perm (HOST
+ * int32[K], perm[new] = old) puts the outliers first by descending score
+ * (ties: ascending channel), the other channels after them in their original
+ * order; block_bits (HOST uint8[K/128]) = 8 for the ceil(#outliers/128)
+ * leading blocks, 4 otherwise (SPEC S:L139-165 rule, theta = 8 there);
+ * *n_outliers (optional) = number of outliers. */
+comet_status comet_calib_absmax(const void* X, int64_t ldx, int32_t M, int32_t K, float* maxabs,
+                                comet_stream_t stream);
+comet_status comet_fmpq_map(const float* score, int32_t K, float theta, int32_t* perm, uint8_t* block_bits,
+                            int32_t* n_outliers);
+
+/* ---- f3: KV4 cache (§3.2, §6.1: "channel-wise asymmetric
+ * INT4 group quantization for the KV cache") ------------------------------
+ * KV fp16 [T x C] (DEVICE; tokens x head-dim channels, row stride ld, C and
+ * ld even).  Per (channel c, group j of `group` consecutive tokens):
+ *   mn, mx = min, max over the group; if mn == mx == v: scale = |v| (1 if
+ *   v == 0), zp = (v < 0); else lo = min(mn, 0), hi = max(mx, 0),
+ *   scale = (hi - lo)/15, zp = clamp(rha(-lo / scale), 0, 15);
+ *   q = clamp(rha(x / scale) + zp, 0, 15)
+ * (IEEE fp32 division, rha = round half away from zero).
+ * Q: DEVICE packed [T x C/2] bytes, byte (t, j) = q[t,2j] | q[t,2j+1] << 4;
+ * scale fp32 / zp uint8: DEVICE [ceil(T/group) x C].
+ * comet_dequantize_kv: out fp16 [T x C] (row stride ldo) = fp16_rn((q - zp) *
+ * scale), the dequantisation an attention kernel applies to the cache. */
+comet_status comet_quantize_kv(const void* KV, int64_t ld, int32_t T, int32_t C, int32_t group, void* Q,
+                               float* scale, uint8_t* zp, comet_stream_t stream);
+comet_status comet_dequantize_kv(const void* Q, const float* scale, const uint8_t* zp, int32_t T, int32_t C,
+                                 int32_t group, void* out, int64_t ldo, comet_stream_t stream);
+
 const char* comet_status_str(comet_status s);
 const char* comet_last_cuda_error(void);
 /* number of kernel launches this library issued since load (host counter) */

@@ -1,0 +1,153 @@
+"""CPU oracle for the FMPQ steps around the W4Ax GEMM -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/`` (and the bench's reference legs) may import this module; the
+product path never does, and nothing here is shared with ``csrc/``.
+
+Definitions, written out plainly from the paper (PAPER.md, arXiv 2410.12168)
+and the SPEC readings listed in DESIGN.md:
+
+* f2 calibration (§3.2, "we first identify channels with outliers
+  through data sampling and then use the permutation strategy to cluster these
+  channels into a single block"; rule from SPEC S:L139-165):
+  score[c] = max over calibration rows |x[m, c]|; median = lower middle of the
+  sorted scores; outlier iff score > theta * median (theta = 8); permutation
+  perm[new] = old with the outliers first by descending score (ties: ascending
+  channel) and the rest in original order; block b (128 channels) is INT8 iff
+  it holds an outlier after the permutation.
+* f3 KV4 (§3.2 "channel-wise 4-bit quantization strategy for the KV
+  cache"; §6.1 "channel-wise asymmetric INT4 group quantization"; the
+  asymmetric min-max rule of SPEC S:L62-70 with its degenerate case):
+  per (channel, group of G tokens): mn, mx; mn == mx == v -> scale = |v| (1 if
+  v == 0), zp = (v < 0); else lo = min(mn, 0), hi = max(mx, 0) (the range
+  holds 0, so the zero point lies in [0, 15] and the round-trip bound holds --
+  DESIGN.md reading), scale = fp32((hi - lo) / 15),
+  zp = clamp(rha(fp32(-lo / scale)), 0, 15); q = clamp(rha(fp32(x / scale)) +
+  zp, 0, 15); dequant = fp16_rne(fp32((q - zp) * scale)).  All divisions and
+  products in IEEE fp32 (the precision the kernels decide the integers in),
+  rha = round half away from zero evaluated exactly.
+
+Parity status: pinned by tests/test_fmpq_aux.py (SPEC worked examples,
+lattice round trips, round-trip bound, brute-force reference of the rules).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+BLOCK = 128
+
+
+# ------------------------------------------------------------------ f2 ----
+def calib_absmax(X: np.ndarray) -> np.ndarray:
+    """Per-channel max |x| over the rows of X (fp16 [M x K]) as fp32 (exact)."""
+    return np.abs(X.astype(np.float32)).max(axis=0)
+
+
+def median_lower(score: np.ndarray) -> float:
+    s = sorted(float(v) for v in score)
+    return s[(len(s) - 1) // 2]
+
+
+def detect_outliers(score: np.ndarray, theta: float = 8.0) -> np.ndarray:
+    """flag iff score > theta * median (theta * median in fp32)."""
+    thr = np.float32(np.float32(theta) * np.float32(median_lower(score)))
+    return np.array([np.float32(v) > thr for v in score], dtype=bool)
+
+
+def build_permutation(score: np.ndarray, flags: np.ndarray) -> np.ndarray:
+    """outliers first by descending score then ascending index,
+    the rest stable.  perm[new] = old."""
+    out = [c for c in range(len(score)) if flags[c]]
+    out.sort(key=lambda c: (-float(score[c]), c))
+    rest = [c for c in range(len(score)) if not flags[c]]
+    return np.array(out + rest, dtype=np.int32)
+
+
+def block_bits_for(perm: np.ndarray, flags: np.ndarray, k: int = BLOCK) -> np.ndarray:
+    """S:L157-165 invariant: block b is 8-bit iff it holds >= 1 outlier."""
+    nb = len(perm) // k
+    return np.array([8 if any(flags[perm[b * k + i]] for i in range(k)) else 4 for b in range(nb)], dtype=np.uint8)
+
+
+def fmpq_map(score: np.ndarray, theta: float = 8.0):
+    flags = detect_outliers(score, theta)
+    perm = build_permutation(score, flags)
+    return perm, block_bits_for(perm, flags), int(flags.sum())
+
+
+# ------------------------------------------------------------------ f3 ----
+def _rha(v: np.float32) -> int:
+    """round half away from zero of an fp32 value (exact: done in fp64)."""
+    a = math.floor(abs(float(v)) + 0.5)
+    return int(a) if v >= 0 else -int(a)
+
+
+def kv_params(mn: np.float32, mx: np.float32):
+    if mn == mx:
+        v = np.float32(mn)
+        return (np.float32(1.0) if v == 0 else np.float32(abs(v))), (1 if v < 0 else 0)
+    lo, hi = np.float32(min(mn, 0)), np.float32(max(mx, 0))  # the range holds 0 (zp in [0, 15])
+    scale = np.float32(np.float32(hi - lo) / np.float32(15.0))
+    zp = min(15, max(0, _rha(np.float32(np.float32(-lo) / scale))))
+    return scale, zp
+
+
+def quantize_kv(KV: np.ndarray, group: int):
+    """KV fp16 [T x C] -> (q uint8 [T x C] unpacked, scale fp32 [G x C], zp uint8 [G x C])."""
+    T, C = KV.shape
+    x = KV.astype(np.float32)
+    ng = (T + group - 1) // group
+    q = np.zeros((T, C), dtype=np.uint8)
+    scale = np.zeros((ng, C), dtype=np.float32)
+    zp = np.zeros((ng, C), dtype=np.uint8)
+    for g in range(ng):
+        t0, t1 = g * group, min(T, (g + 1) * group)
+        for c in range(C):
+            col = x[t0:t1, c]
+            s, z = kv_params(np.float32(col.min()), np.float32(col.max()))
+            scale[g, c], zp[g, c] = s, z
+            for t in range(t0, t1):
+                q[t, c] = min(15, max(0, _rha(np.float32(col[t - t0] / s)) + z))
+    return q, scale, zp
+
+
+def quantize_kv_vec(KV: np.ndarray, group: int):
+    """Same definition, vectorised over channels (for larger test sizes);
+    pinned against quantize_kv on small inputs."""
+    T, C = KV.shape
+    x = KV.astype(np.float32)
+    ng = (T + group - 1) // group
+    q = np.zeros((T, C), dtype=np.uint8)
+    scale = np.zeros((ng, C), dtype=np.float32)
+    zp = np.zeros((ng, C), dtype=np.uint8)
+    for g in range(ng):
+        t0, t1 = g * group, min(T, (g + 1) * group)
+        blk = x[t0:t1]
+        mn, mx = blk.min(axis=0), blk.max(axis=0)
+        deg = mn == mx
+        lo, hi = np.minimum(mn, 0).astype(np.float32), np.maximum(mx, 0).astype(np.float32)
+        s = np.where(deg, np.where(mn == 0, np.float32(1), np.abs(mn)),
+                     ((hi - lo).astype(np.float32) / np.float32(15)).astype(np.float32)).astype(np.float32)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            zr = (-lo).astype(np.float32) / s
+        zr64 = zr.astype(np.float64)
+        z = np.where(deg, (mn < 0).astype(np.int64),
+                     np.clip(np.sign(zr64) * np.floor(np.abs(zr64) + 0.5), 0, 15).astype(np.int64))
+        scale[g], zp[g] = s, z
+        v = (blk / s).astype(np.float32).astype(np.float64)
+        r = np.sign(v) * np.floor(np.abs(v) + 0.5)
+        q[t0:t1] = np.clip(r + z, 0, 15).astype(np.uint8)
+    return q, scale, zp
+
+
+def pack_kv(q: np.ndarray) -> np.ndarray:
+    """[T x C] nibbles -> [T x C/2] bytes, byte j = q[2j] | q[2j+1] << 4."""
+    return (q[:, 0::2] | (q[:, 1::2] << 4)).astype(np.uint8)
+
+
+def dequantize_kv(q: np.ndarray, scale: np.ndarray, zp: np.ndarray, group: int) -> np.ndarray:
+    T, C = q.shape
+    g = np.arange(T) // group
+    y = ((q.astype(np.float32) - zp[g].astype(np.float32)).astype(np.float32) * scale[g]).astype(np.float32)
+    return y.astype(np.float16)

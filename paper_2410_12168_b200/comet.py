@@ -68,6 +68,14 @@ def lib():
         L.comet_w4ax_gemm_acc_i32.restype = ctypes.c_int
         L.comet_w4ax_linear.argtypes = [P, i64, i32, i32, P, P, P, P, i32, i32, P, i64, P, sz, P]
         L.comet_w4ax_linear.restype = ctypes.c_int
+        L.comet_calib_absmax.argtypes = [P, i64, i32, i32, P, P]
+        L.comet_calib_absmax.restype = ctypes.c_int
+        L.comet_fmpq_map.argtypes = [P, i32, ctypes.c_float, P, P, P]
+        L.comet_fmpq_map.restype = ctypes.c_int
+        L.comet_quantize_kv.argtypes = [P, i64, i32, i32, i32, P, P, P, P]
+        L.comet_quantize_kv.restype = ctypes.c_int
+        L.comet_dequantize_kv.argtypes = [P, P, P, i32, i32, i32, P, i64, P]
+        L.comet_dequantize_kv.restype = ctypes.c_int
         L.comet_status_str.argtypes = [ctypes.c_int]
         L.comet_status_str.restype = ctypes.c_char_p
         L.comet_last_cuda_error.argtypes = []
@@ -180,6 +188,56 @@ def comet_quantize_act(X: torch.Tensor, bits, perm: Optional[torch.Tensor] = Non
                                   _ptr(Xq4) if b.n4 else None, _ptr(Sx), Sx.shape[1], _stream(stream))
     _check("comet_quantize_act", st)
     return Xq8, Xq4, Sx
+
+
+def comet_calib_absmax(X: torch.Tensor, maxabs: Optional[torch.Tensor] = None, stream=None):
+    """f2: per-channel max |X| over the rows of X fp16 [M x K], accumulated
+    into maxabs (DEVICE fp32[K], zero-initialised when None)."""
+    assert X.is_cuda and X.dtype == torch.float16 and X.dim() == 2 and X.stride(1) == 1
+    M, K = X.shape
+    if maxabs is None:
+        maxabs = torch.zeros(K, dtype=torch.float32, device=X.device)
+    st = lib().comet_calib_absmax(_ptr(X), X.stride(0), M, K, _ptr(maxabs), _stream(stream))
+    _check("comet_calib_absmax", st)
+    return maxabs
+
+
+def comet_fmpq_map(score, theta: float = 8.0):
+    """f2 (host): per-channel scores -> (perm int32[K], block_bits uint8[K/128],
+    number of outliers), the SPEC S:L139-165 rule (see comet.h)."""
+    import numpy as np
+    sc = np.ascontiguousarray(np.asarray(score.cpu() if hasattr(score, "cpu") else score, dtype=np.float32))
+    K = sc.shape[0]
+    perm = np.empty(K, dtype=np.int32)
+    bits = np.empty(K // BLOCK, dtype=np.uint8)
+    n = ctypes.c_int32(0)
+    st = lib().comet_fmpq_map(sc.ctypes.data, K, float(theta), perm.ctypes.data, bits.ctypes.data, ctypes.byref(n))
+    _check("comet_fmpq_map", st)
+    return perm, bits, int(n.value)
+
+
+def comet_quantize_kv(KV: torch.Tensor, group: int, stream=None):
+    """f3: KV fp16 [T x C] -> (Q uint8 [T x C/2] packed, scale fp32 [G x C],
+    zp uint8 [G x C]), G = ceil(T / group)."""
+    assert KV.is_cuda and KV.dtype == torch.float16 and KV.dim() == 2 and KV.stride(1) == 1
+    T, C = KV.shape
+    ng = (T + group - 1) // group
+    Q = torch.empty((T, C // 2), dtype=torch.uint8, device=KV.device)
+    scale = torch.empty((ng, C), dtype=torch.float32, device=KV.device)
+    zp = torch.empty((ng, C), dtype=torch.uint8, device=KV.device)
+    st = lib().comet_quantize_kv(_ptr(KV), KV.stride(0), T, C, group, _ptr(Q), _ptr(scale), _ptr(zp), _stream(stream))
+    _check("comet_quantize_kv", st)
+    return Q, scale, zp
+
+
+def comet_dequantize_kv(Q: torch.Tensor, scale: torch.Tensor, zp: torch.Tensor, group: int, stream=None):
+    """f3: packed KV4 -> fp16 [T x C]."""
+    T, C = Q.shape[0], Q.shape[1] * 2
+    out = torch.empty((T, C), dtype=torch.float16, device=Q.device)
+    st = lib().comet_dequantize_kv(_ptr(Q), _ptr(scale), _ptr(zp), T, C, group, _ptr(out), out.stride(0),
+                                   _stream(stream))
+    _check("comet_dequantize_kv", st)
+    return out
 
 
 def comet_w4ax_gemm(Xq8, Xq4, Sx, bits, Wq, Sw, group: int = BLOCK, out: Optional[torch.Tensor] = None,

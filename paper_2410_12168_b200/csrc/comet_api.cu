@@ -8,11 +8,14 @@
 
 #include <atomic>
 #include <mutex>
+#include <algorithm>
+#include <vector>
 
 #include "../../include/comet.h"
 #include "gemm.cuh"
 #include "gemm_2sm.cuh"
 #include "gemm_pf.cuh"
+#include "fmpq_aux.cuh"
 #include "gemm_decode.cuh"
 #include "quantize.cuh"
 
@@ -578,6 +581,82 @@ const char* comet_status_str(comet_status s) {
 }
 
 const char* comet_last_cuda_error(void) { return g_cuda_err; }
+
+// ---- f2: calibration ("identify channels with outliers through data
+// sampling") ------------------------------------------------------------------
+comet_status comet_calib_absmax(const void* X, int64_t ldx, int32_t M, int32_t K, float* maxabs,
+                                comet_stream_t stream) {
+  if (M < 0 || K <= 0) return COMET_ERR_INVALID_ARG;
+  if (K % 8 || ldx < K || ldx % 8) return COMET_ERR_SHAPE;
+  if (M == 0) return COMET_OK;
+  if (!X || !maxabs) return COMET_ERR_INVALID_ARG;
+  if (!aligned16(X) || (reinterpret_cast<uintptr_t>(maxabs) & 3)) return COMET_ERR_ALIGNMENT;
+  comet_status ds = device_check(nullptr);
+  if (ds != COMET_OK) return ds;
+  // x: 256-channel slices; y: row groups of 8, sized so the grid is ~8 CTAs per SM
+  const int xs = (K + 255) / 256;
+  int ys = (148 * 8 + xs - 1) / xs;
+  if (ys > (M + 7) / 8) ys = (M + 7) / 8;
+  const dim3 grid((unsigned)xs, (unsigned)ys);
+  calib_absmax_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const __half*>(X), ldx, M, K, maxabs);
+  return check_launch();
+}
+
+comet_status comet_fmpq_map(const float* score, int32_t K, float theta, int32_t* perm, uint8_t* block_bits,
+                            int32_t* n_outliers) {
+  if (!score || !perm || !block_bits || K <= 0 || !(theta > 1.0f)) return COMET_ERR_INVALID_ARG;
+  if (K % COMET_BLOCK) return COMET_ERR_SHAPE;
+  for (int32_t c = 0; c < K; ++c)
+    if (!(score[c] >= 0.0f) || score[c] == INFINITY) return COMET_ERR_INVALID_ARG;  // non-finite or negative
+  std::vector<float> sorted(score, score + K);
+  std::sort(sorted.begin(), sorted.end());
+  const float median = sorted[(K - 1) / 2];  // lower middle for even K
+  const float thr = theta * median;
+  std::vector<int32_t> out, rest;
+  for (int32_t c = 0; c < K; ++c) (score[c] > thr ? out : rest).push_back(c);
+  // outliers first by descending score, ties by ascending channel; the rest stable
+  std::stable_sort(out.begin(), out.end(), [&](int32_t a, int32_t b) { return score[a] > score[b]; });
+  int32_t i = 0;
+  for (int32_t c : out) perm[i++] = c;
+  for (int32_t c : rest) perm[i++] = c;
+  const int32_t n8 = ((int32_t)out.size() + COMET_BLOCK - 1) / COMET_BLOCK;
+  for (int32_t b = 0; b < K / COMET_BLOCK; ++b) block_bits[b] = b < n8 ? 8 : 4;
+  if (n_outliers) *n_outliers = (int32_t)out.size();
+  return COMET_OK;
+}
+
+// ---- f3: KV4 cache ("channel-wise asymmetric INT4 group
+// quantization for the KV cache") ---------------------------------------------
+comet_status comet_quantize_kv(const void* KV, int64_t ld, int32_t T, int32_t C, int32_t group, void* Q,
+                               float* scale, uint8_t* zp, comet_stream_t stream) {
+  if (T < 0 || C <= 0 || group <= 0) return COMET_ERR_INVALID_ARG;
+  if (C % 2 || ld < C || ld % 2) return COMET_ERR_SHAPE;
+  if (T == 0) return COMET_OK;
+  if (!KV || !Q || !scale || !zp) return COMET_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(KV) & 3) || (reinterpret_cast<uintptr_t>(scale) & 3)) return COMET_ERR_ALIGNMENT;
+  comet_status ds = device_check(nullptr);
+  if (ds != COMET_OK) return ds;
+  const dim3 grid((unsigned)((C / 2 + 63) / 64), (unsigned)((T + group - 1) / group));
+  kv4_quantize_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const __half*>(KV), ld, T, C, group, reinterpret_cast<uint8_t*>(Q), scale, zp);
+  return check_launch();
+}
+
+comet_status comet_dequantize_kv(const void* Q, const float* scale, const uint8_t* zp, int32_t T, int32_t C,
+                                 int32_t group, void* out, int64_t ldo, comet_stream_t stream) {
+  if (T < 0 || C <= 0 || group <= 0) return COMET_ERR_INVALID_ARG;
+  if (C % 2 || ldo < C || ldo % 2) return COMET_ERR_SHAPE;
+  if (T == 0) return COMET_OK;
+  if (!Q || !scale || !zp || !out) return COMET_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(out) & 3) || (reinterpret_cast<uintptr_t>(scale) & 3)) return COMET_ERR_ALIGNMENT;
+  comet_status ds = device_check(nullptr);
+  if (ds != COMET_OK) return ds;
+  const int64_t units = (int64_t)T * (C / 2);
+  kv4_dequantize_kernel<<<(unsigned)((units + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const uint8_t*>(Q), scale, zp, T, C, group, reinterpret_cast<__half*>(out), ldo);
+  return check_launch();
+}
 
 // debug only (not part of comet.h): enable/read per-CTA timestamps of the
 // decode kernel, [start_ns, end_ns, smid] x n

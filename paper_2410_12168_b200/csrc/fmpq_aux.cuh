@@ -1,0 +1,160 @@
+// fmpq_aux.cuh -- the two FMPQ steps around the W4Ax GEMM:
+//   f2  calibration: per-channel absmax over calibration activations, the
+//       score that identifies outlier channels "through data sampling"
+//       (§3.2); the permutation / block mask are built on the host
+//       (comet_fmpq_map in comet_api.cu);
+//   f3  KV4: "channel-wise asymmetric INT4 group quantization for the KV
+//       cache" (§6.1, §3.2) -- quantize-on-append and the
+//       dequantization an attention kernel applies.
+// All HBM-bound streaming kernels (coalesced 16-byte / 4-byte accesses).
+#pragma once
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "quantize.cuh"
+#include "sm100.cuh"
+
+namespace comet {
+
+// maxabs[c] = max(maxabs[c], max_m |X[m, c]|).  CTA = 32 channel octets (one
+// warp-wide 512-byte row segment per load) x 8 row lanes; rows
+// 8 * blockIdx.y + lane8, strided by 8 * gridDim.y; the 8 row lanes are
+// reduced in shared memory and merged across CTAs with one integer atomicMax
+// per channel on the fp32 bit pattern (order-independent, exact for
+// non-negative floats).
+__global__ void __launch_bounds__(256) calib_absmax_kernel(const __half* __restrict__ X, int64_t ldx, int M, int K,
+                                                           float* __restrict__ maxabs) {
+  __shared__ float red[8][32 * 8 + 1];
+  const int lane = threadIdx.x & 31, rl = threadIdx.x >> 5;  // octet lane, row lane
+  const int oct = blockIdx.x * 32 + lane;
+  const bool live = oct * 8 < K;
+  float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (live) {
+    for (int64_t m = (int64_t)blockIdx.y * 8 + rl; m < M; m += (int64_t)gridDim.y * 8) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(X + m * ldx + oct * 8));
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        a[2 * j] = fmaxf(a[2 * j], fabsf(half_bits_to_float(w[j] & 0xFFFF)));
+        a[2 * j + 1] = fmaxf(a[2 * j + 1], fabsf(half_bits_to_float(w[j] >> 16)));
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) red[rl][lane * 8 + j] = a[j];
+  __syncthreads();
+  // thread t merges channel t of this CTA's 256 channels over the 8 row lanes
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c < K) {
+    float v = red[0][threadIdx.x];
+#pragma unroll
+    for (int r = 1; r < 8; ++r) v = fmaxf(v, red[r][threadIdx.x]);
+    atomicMax(reinterpret_cast<unsigned int*>(maxabs) + c, __float_as_uint(v));
+  }
+}
+
+// KV4 quantization of one token group: thread = channel pair (2j, 2j+1)
+// (one 4-byte half2 load per token, one packed byte per token out).
+// Asymmetric INT4 per (channel, group of G tokens):
+//   mn, mx = min, max over the group;  mn == mx == v: scale = |v| (1 if v == 0),
+//   zp = (v < 0);  else lo = min(mn, 0), hi = max(mx, 0), scale = (hi - lo) / 15,
+//   zp = clamp(rha(-lo / scale), 0, 15);
+//   q = clamp(rha(x / scale) + zp, 0, 15)  (IEEE fp32, rha = round half away).
+DEVI void kv_params(float mn, float mx, float& scale, int& zp) {
+  if (mn == mx) {
+    scale = mn == 0.0f ? 1.0f : fabsf(mn);
+    zp = mn < 0.0f ? 1 : 0;
+  } else {
+    // the range holds 0 so the zero point lies in [0, 15] (DESIGN.md reading)
+    const float lo = fminf(mn, 0.0f), hi = fmaxf(mx, 0.0f);
+    scale = __fdiv_rn(__fsub_rn(hi, lo), 15.0f);
+    zp = min(15, max(0, round_half_away(__fdiv_rn(-lo, scale))));
+  }
+}
+
+// CTA = one token group x 64 channel pairs, 4 token lanes per pair (256
+// threads): min/max over the group reduced across the token lanes in shared
+// memory, then every thread quantizes its tokens t0 + lane4, +4, ...
+__global__ void __launch_bounds__(256) kv4_quantize_kernel(const __half* __restrict__ KV, int64_t ld, int T, int C,
+                                                           int G, uint8_t* __restrict__ Q, float* __restrict__ scale,
+                                                           uint8_t* __restrict__ zp) {
+  __shared__ float red[4][4][64];  // [min0, max0, min1, max1][token lane][pair]
+  const int pl = threadIdx.x & 63, tl = threadIdx.x >> 6;
+  const int pr = blockIdx.x * 64 + pl;  // channel pair
+  const bool live = 2 * pr < C;
+  const int g = blockIdx.y;
+  const int t0 = g * G, t1 = min(T, t0 + G);
+  float mn0 = INFINITY, mx0 = -INFINITY, mn1 = INFINITY, mx1 = -INFINITY;
+  if (live) {
+    for (int t = t0 + tl; t < t1; t += 4) {
+      const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(KV + (int64_t)t * ld + 2 * pr));
+      const float x0 = half_bits_to_float(w & 0xFFFF), x1 = half_bits_to_float(w >> 16);
+      mn0 = fminf(mn0, x0);
+      mx0 = fmaxf(mx0, x0);
+      mn1 = fminf(mn1, x1);
+      mx1 = fmaxf(mx1, x1);
+    }
+  }
+  red[0][tl][pl] = mn0;
+  red[1][tl][pl] = mx0;
+  red[2][tl][pl] = mn1;
+  red[3][tl][pl] = mx1;
+  __syncthreads();
+  mn0 = fminf(fminf(red[0][0][pl], red[0][1][pl]), fminf(red[0][2][pl], red[0][3][pl]));
+  mx0 = fmaxf(fmaxf(red[1][0][pl], red[1][1][pl]), fmaxf(red[1][2][pl], red[1][3][pl]));
+  mn1 = fminf(fminf(red[2][0][pl], red[2][1][pl]), fminf(red[2][2][pl], red[2][3][pl]));
+  mx1 = fmaxf(fmaxf(red[3][0][pl], red[3][1][pl]), fmaxf(red[3][2][pl], red[3][3][pl]));
+  if (!live) return;
+  float s0, s1;
+  int z0, z1;
+  kv_params(mn0, mx0, s0, z0);
+  kv_params(mn1, mx1, s1, z1);
+  if (tl == 0) {
+    scale[(int64_t)g * C + 2 * pr] = s0;
+    scale[(int64_t)g * C + 2 * pr + 1] = s1;
+    zp[(int64_t)g * C + 2 * pr] = (uint8_t)z0;
+    zp[(int64_t)g * C + 2 * pr + 1] = (uint8_t)z1;
+  }
+  for (int t = t0 + tl; t < t1; t += 4) {
+    const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(KV + (int64_t)t * ld + 2 * pr));
+    const float x0 = half_bits_to_float(w & 0xFFFF), x1 = half_bits_to_float(w >> 16);
+    const int q0 = min(15, max(0, round_half_away(__fdiv_rn(x0, s0)) + z0));
+    const int q1 = min(15, max(0, round_half_away(__fdiv_rn(x1, s1)) + z1));
+    Q[(int64_t)t * (C / 2) + pr] = (uint8_t)(q0 | (q1 << 4));
+  }
+}
+
+// out[t, c] = fp16_rn((q - zp) * scale) for every token t and channel c.
+// Thread = 8 packed bytes (16 channels) of one token when C % 16 == 0
+// (8-byte load, 32-byte store), else one byte.
+__global__ void __launch_bounds__(256) kv4_dequantize_kernel(const uint8_t* __restrict__ Q,
+                                                             const float* __restrict__ scale,
+                                                             const uint8_t* __restrict__ zp, int T, int C, int G,
+                                                             __half* __restrict__ out, int64_t ldo) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int per = 1;  // bytes per thread (8-byte variant measured slower: serial parameter loads)
+  const int64_t units = (int64_t)T * (C / 2) / per;
+  if (i >= units) return;
+  const int64_t byte0 = i * per;
+  const int t = (int)(byte0 / (C / 2)), pr0 = (int)(byte0 % (C / 2));
+  const int64_t prow = (int64_t)(t / G) * C;
+  uint32_t bytes[8];
+  if (per == 8) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(Q + byte0));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      bytes[j] = (v.x >> (8 * j)) & 0xFF;
+      bytes[4 + j] = (v.y >> (8 * j)) & 0xFF;
+    }
+  } else {
+    bytes[0] = Q[byte0];
+  }
+  for (int j = 0; j < per; ++j) {
+    const int c = 2 * (pr0 + j);
+    const float y0 = __fmul_rn((float)((int)(bytes[j] & 0xF) - (int)zp[prow + c]), scale[prow + c]);
+    const float y1 = __fmul_rn((float)((int)(bytes[j] >> 4) - (int)zp[prow + c + 1]), scale[prow + c + 1]);
+    *reinterpret_cast<__half2*>(out + (int64_t)t * ldo + c) = __halves2half2(__float2half_rn(y0), __float2half_rn(y1));
+  }
+}
+
+}  // namespace comet

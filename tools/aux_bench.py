@@ -1,0 +1,63 @@
+"""Time the FMPQ side kernels with CUDA events, L2 flushed.
+
+    python tools/aux_bench.py   -> one JSON line per kernel (GB/s vs measured HBM peak)
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+from paper_2410_12168_b200 import comet
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def peak():
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(d.get("hbm_gbs") or d.get("hbm_copy_gbs"))
+    except Exception:
+        return 6650.0
+
+
+def timed(fn, reps=20):
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    ts = []
+    for i in range(reps + 3):
+        flush.fill_(1)
+        torch.cuda._sleep(1_000_000)
+        a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+        a.record(); fn(); b.record()
+        torch.cuda.synchronize()
+        if i >= 3:
+            ts.append(a.elapsed_time(b) * 1e-3)
+    return float(np.median(ts))
+
+
+def main():
+    pk = peak()
+    out = []
+    # f2: calibration absmax over a 4096-token batch of a K=8192 activation
+    X = torch.randn(4096, 8192, device="cuda").half()
+    acc = torch.zeros(8192, device="cuda")
+    t = timed(lambda: comet.comet_calib_absmax(X, acc))
+    out.append({"kernel": "calib_absmax", "shape": [4096, 8192], "us": t * 1e6, "GBs": X.numel() * 2 / t / 1e9})
+    # f3: KV4 quantize-on-append of a prefill chunk: 8192 tokens x (8 kv heads x 128 dims), group 128
+    KV = torch.randn(8192, 1024, device="cuda").half()
+    t = timed(lambda: comet.comet_quantize_kv(KV, 128))
+    byts = KV.numel() * 2 + KV.numel() // 2 + 8192 // 128 * 1024 * 5
+    out.append({"kernel": "kv4_quantize", "shape": [8192, 1024, 128], "us": t * 1e6, "GBs": byts / t / 1e9})
+    Q, s, z = comet.comet_quantize_kv(KV, 128)
+    t = timed(lambda: comet.comet_dequantize_kv(Q, s, z, 128))
+    byts = KV.numel() // 2 + KV.numel() * 2 + 8192 // 128 * 1024 * 5
+    out.append({"kernel": "kv4_dequantize", "shape": [8192, 1024, 128], "us": t * 1e6, "GBs": byts / t / 1e9})
+    for o in out:
+        o["frac_of_hbm"] = o["GBs"] / pk
+        print(json.dumps(o))
+
+
+if __name__ == "__main__":
+    main()
