@@ -23,7 +23,8 @@ STATUS = {0: "COMET_OK", 1: "COMET_ERR_INVALID_ARG", 2: "COMET_ERR_SHAPE", 3: "C
           4: "COMET_ERR_WORKSPACE", 5: "COMET_ERR_UNSUPPORTED", 6: "COMET_ERR_CUDA"}
 EXPORTS = ["comet_act_plane8_bytes", "comet_act_plane4_bytes", "comet_act_ldsx", "comet_w4ax_gemm_workspace_bytes",
            "comet_w4ax_linear_scratch_bytes", "comet_pack_weight", "comet_quantize_act", "comet_w4ax_gemm",
-           "comet_w4ax_gemm_acc_i32", "comet_w4ax_linear", "comet_status_str", "comet_last_cuda_error",
+           "comet_w4ax_gemm_acc_i32", "comet_w4ax_linear", "comet_calib_absmax", "comet_fmpq_map",
+           "comet_quantize_kv", "comet_dequantize_kv", "comet_status_str", "comet_last_cuda_error",
            "comet_launch_count"]
 
 
