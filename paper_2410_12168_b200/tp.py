@@ -47,3 +47,46 @@ def gathered_to_full(y_all: torch.Tensor, N: int) -> torch.Tensor:
     """[P x M x width] rank-major shards -> [M x N] (drops the padding)."""
     P, M, per = y_all.shape
     return y_all.permute(1, 0, 2).reshape(M, P * per)[:, :N]
+
+
+# ------------------------------------------- SURVEY 8(f) f1: overlap ----
+def chunk_bounds(M: int, chunks: int):
+    """[(m0, m1)] splitting M rows into `chunks` near-equal contiguous ranges."""
+    chunks = max(1, min(chunks, M)) if M > 0 else 1
+    edges = [M * i // chunks for i in range(chunks + 1)]
+    return [(edges[i], edges[i + 1]) for i in range(chunks) if edges[i + 1] > edges[i]]
+
+
+def pipelined_linear_allgather(gemm_rows, M: int, per: int, chunks: int, dtype, device, group=None):
+    """GEMM + all-gather with the exchange of row chunk i overlapping the GEMM
+    of chunk i + 1 (the "overlapped" column of SURVEY 8(e): serial
+    GEMM + AG -> max(GEMM, AG) when the chunks pipeline).
+
+    gemm_rows(m0, m1, out) writes rows [m0, m1) of this rank's Y shard into
+    out ([m1 - m0, per], contiguous) on the current stream.  Each chunk's
+    all_gather is issued asynchronously right after its GEMM (NCCL runs it on
+    its own stream after the GEMM's event; gloo on a helper thread), so the
+    next chunk's GEMM is enqueued while the previous chunk is in flight.
+    Returns (y_chunks, bounds): y_chunks[i] is [P, m1 - m0, per] (rank-major)
+    and lives in one flat buffer; chunked_to_full reassembles [M x N].
+    """
+    world = dist.get_world_size(group)
+    bounds = chunk_bounds(M, chunks)
+    y_local = torch.empty((M, per), dtype=dtype, device=device)
+    flat = torch.empty(world * M * per, dtype=dtype, device=device)
+    y_chunks, works = [], []
+    for m0, m1 in bounds:
+        mc = m1 - m0
+        gemm_rows(m0, m1, y_local[m0:m1])
+        dst = flat[world * m0 * per: world * m1 * per].view(world, mc, per)
+        works.append(dist.all_gather_into_tensor(dst.view(world * mc, per), y_local[m0:m1], group=group,
+                                                 async_op=True))
+        y_chunks.append(dst)
+    for w in works:
+        w.wait()
+    return y_chunks, bounds
+
+
+def chunked_to_full(y_chunks, bounds, N: int) -> torch.Tensor:
+    """[P x mc x per] rank-major chunks -> [M x N] (drops the padding)."""
+    return torch.cat([gathered_to_full(yc, N) for yc in y_chunks], dim=0)

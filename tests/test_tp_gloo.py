@@ -85,3 +85,56 @@ def test_gathered_to_full_layout():
     y_all = torch.arange(2 * 3 * 4).reshape(2, 3, 4)
     full = tp.gathered_to_full(y_all, 7)
     assert full.tolist() == [[0, 1, 2, 3, 12, 13, 14], [4, 5, 6, 7, 16, 17, 18], [8, 9, 10, 11, 20, 21, 22]]
+
+
+def _worker_pipelined(rank, world, port, M, N, K, chunks, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = synth.make_problem(M, N, K, n8=1, seed=37)
+        Wl = tp.shard_weight(p["W"], world, rank)
+        n0, n1, per = tp.shard_rows(N, world, rank)
+        Xq8, Xq4, Sx = oracle.quantize_act(p["X"], p["bits"], p["perm"])
+        Wq, Sw = oracle.pack_weight(Wl, 128, p["perm"])
+        y = oracle.w4ax_gemm(Xq8, Xq4, Sx, p["bits"], Wq, Sw, group=128)["y"]
+        calls = []
+
+        def gemm_rows(m0, m1, out):  # stand-in for the device GEMM of rows [m0, m1)
+            calls.append((m0, m1))
+            out.copy_(torch.from_numpy(y[m0:m1].astype(np.float32)))
+
+        yc, bounds = tp.pipelined_linear_allgather(gemm_rows, M, per, chunks, torch.float32, "cpu")
+        full = tp.chunked_to_full(yc, bounds, N).numpy().astype(np.float16)
+        q.put((rank, full, calls))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 4])
+def test_pipelined_gemm_allgather_equals_single_process(chunks):
+    """f1: the chunked GEMM/all-gather pipeline reassembles the same Y."""
+    M, N, K, world = 10, 640, 256, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_pipelined, args=(r, world, port, M, N, K, chunks, q)) for r in range(world)]
+    for p_ in procs:
+        p_.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    p = synth.make_problem(M, N, K, n8=1, seed=37)
+    Xq8, Xq4, Sx = oracle.quantize_act(p["X"], p["bits"], p["perm"])
+    Wq, Sw = oracle.pack_weight(p["W"], 128, p["perm"])
+    ref = oracle.w4ax_gemm(Xq8, Xq4, Sx, p["bits"], Wq, Sw, group=128)["y"]
+    for rank, full, calls in res:
+        assert np.array_equal(full.view(np.uint16), ref.view(np.uint16)), rank
+        assert calls == tp.chunk_bounds(M, chunks)
+
+
+def test_chunk_bounds():
+    assert tp.chunk_bounds(10, 3) == [(0, 3), (3, 6), (6, 10)]
+    assert tp.chunk_bounds(2, 4) == [(0, 1), (1, 2)]
+    assert tp.chunk_bounds(7, 1) == [(0, 7)]
