@@ -30,6 +30,25 @@ comet_status cuda_fail(cudaError_t e) {
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
   return COMET_ERR_CUDA;
 }
+// launch with the programmatic-stream-serialization (PDL) attribute: the
+// kernel may start while its predecessor in the stream still runs; every
+// GEMM kernel waits (griddepcontrol.wait) before touching data a predecessor
+// may produce
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 comet_status check_launch() {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
@@ -218,7 +237,8 @@ comet_status launch_gemm_pf(const CUtensorMap& tmX4, const CUtensorMap& tmX8, co
   sched.tiles = p.m_tiles * ((args.N + C::kTileN - 1) / C::kTileN);
   sched.clusters = sched.tiles < p.clusters ? sched.tiles : p.clusters;
   dim3 grid(2 * sched.clusters, 1, 1);
-  kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(tmY, tmX4, tmX8, map, args, sched);
+  cudaError_t e = launch_pdl(kern, grid, dim3(C::kThreads), C::kSmemBytes, st, tmY, tmX4, tmX8, map, args, sched);
+  if (e != cudaSuccess) return cuda_fail(e);
   return check_launch();
 }
 
@@ -240,7 +260,9 @@ comet_status launch_decode(const DecMaps& dm, const CUtensorMap& tmX4, const CUt
   sched.tiles = p.n_tiles * p.m_tiles;
   sched.units = sched.tiles * args.nb;  // K-blocks: the split granularity
   sched.ctas = p.clusters;
-  kern<<<sched.ctas, C::kThreads, C::kSmemBytes, st>>>(dm.sx, tmX4, tmX8, dm.sw, map, args, sched);
+  cudaError_t e = launch_pdl(kern, dim3(sched.ctas), dim3(C::kThreads), C::kSmemBytes, st, dm.sx, tmX4, tmX8, dm.sw,
+                             map, args, sched);
+  if (e != cudaSuccess) return cuda_fail(e);
   return check_launch();
 }
 

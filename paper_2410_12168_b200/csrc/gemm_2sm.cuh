@@ -162,6 +162,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
 
   if (warp == C::kLoadWarp) {
     // ------------------------------------------------- a3: producer ----
+    grid_dep_wait();  // PDL: operands come from the preceding kernels
     int t = cluster, b = 0;
     int m0 = 0, n0 = 0;
     sched.coords(t, m0, n0);

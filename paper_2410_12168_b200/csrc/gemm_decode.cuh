@@ -223,6 +223,16 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
     const uint64_t pol_w = l2_policy_evict_first();
     RoleTimer rt(g_cta_times_on && blockIdx.x + 1 == g_cta_times_on && lane == 0);
     int i = 0;
+    // PDL: while the quantizer that precedes this GEMM still runs, warm L2 with
+    // the first units' weights (an L2 prefetch cannot expose stale data: L2 is
+    // the point of coherence), then wait for the predecessor before any load
+    // into shared memory (the weights may have been written by it)
+    if (elect_one()) {
+      int k = 0;
+      for (It it(u0, u1, nb, sched.n_tiles); it.valid() && k < C::kWStages; it.next(nb), ++k)
+        bulk_prefetch_l2(args.Wq + ((int64_t)it.tn * nb + it.b) * 8192, it.len * 8192);
+    }
+    grid_dep_wait();
     for (It it(u0, u1, nb, sched.n_tiles); it.valid(); it.next(nb), ++i) {
       const int s = i % C::kWStages;
       rt.wait(&wempty[s], ((i / C::kWStages) & 1) ^ 1, 0);
@@ -238,6 +248,7 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
     rt.flush(0);
   } else if (warp == 2) {
     // ---------------------------------- a3: token + scale producer ----
+    grid_dep_wait();  // PDL: the planes and scales come from the preceding quantizer
     const bool tr_on = g_cta_times_on && blockIdx.x + 1 == g_cta_times_on && lane == 0;
     int i = 0;
     for (It it(u0, u1, nb, sched.n_tiles); it.valid(); it.next(nb), ++i) {

@@ -217,8 +217,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
     // two warps: each TMA / bulk-copy issue costs the issuing thread ~10^2
     // cycles, and one thread issuing all of a block's copies was the rate limit
     const bool wrole = warp == C::kLoadWarp;
+    // PDL: the token producer waits for the preceding quantizer before its
+    // first load; the weight producer first warms L2 with its first blocks
+    // (cannot expose stale data), then waits too (the weights may have been
+    // written by the predecessor)
     int pg = 0, pt = cluster, pb = 0, pm0 = 0, pn0 = 0;
     sched.coords(pt, pm0, pn0);
+    if (wrole && elect_one() && pt < sched.tiles) {
+      const int R = pn0 + C::kRows * (int)crank;
+      const int v = max(0, min(C::kRows, args.N - R));
+      for (int b = 0; b < min(nb, C::kLStages + C::kStages); ++b)
+        for (int r = R, left = v; left > 0;) {
+          const int in_slab = min(left, 128 - (r & 127));
+          bulk_prefetch_l2(args.Wq + ((int64_t)(r >> 7) * nb + b) * 8192 + (r & 127) * 64, in_slab * 64);
+          r += in_slab;
+          left -= in_slab;
+        }
+    }
+    __syncwarp();
+    grid_dep_wait();
     for (; pg < steps;) {
       const int g = pg, b = pb;
       const int l = g % C::kLStages;

@@ -513,6 +513,13 @@ DEVI uint32_t opaque(uint32_t v) {
   return v;
 }
 
+// programmatic dependent launch: a kernel launched with the PDL stream
+// attribute may start while its predecessor runs; griddepcontrol.wait blocks
+// until the predecessor grid has completed and its memory is visible.  The
+// predecessor lets dependents get scheduled early with launch_dependents.
+DEVI void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+DEVI void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // per-warpgroup register budget (all 4 warps of the warpgroup execute it)
 template <int N>
 DEVI void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
