@@ -81,6 +81,11 @@ DEVI void pf_wait_cluster(uint64_t* bar, uint32_t parity) {
 #define COMET_PF_EXP 0  // timing experiments only (wrong results): 1 = skip staging work, 2 = skip promotion math, 3 = both, 4 = also skip the accumulator loads, 5 = also skip the operand loads
 #endif
 
+#ifndef COMET_PF_REGS
+#define COMET_PF_REGS 0  // 1: setmaxnreg rebalancing (promotion 120 / staging 64 / producers+MMA 40); ptxas
+                         // still pipelines the accumulator loads 3 deep, so no gain -- and the pool is the
+                         // launch allocation (96 x 640), not 64K: a larger inc deadlocks
+#endif
 #ifndef COMET_PF_LDPIPE
 #define COMET_PF_LDPIPE 1  // double-buffered 8-column accumulator loads in the promotion
 #endif
@@ -212,28 +217,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
   // debug trace of one CTA (COMET_TRACE builds; tools/gemm_sweep.py trace3)
   const bool tr_cta = kTraceBuild && g_cta_times_on && blockIdx.x + 1 == g_cta_times_on;
 
+  // register rebalancing per warpgroup (the launch pool 96 x 640 = 3 x 128 x 120
+  // + 128 x 64 + 128 x 40 + slack; every warp of a warpgroup executes the same setmaxnreg, inside
+  // the warpgroup's branch so ptxas allocates each role's code to its budget):
+  // the promotion warps hold the running sums (64) and 7 accumulator chunks
+  if (warp >= 16) {
+  if (COMET_PF_REGS) setmaxnreg_dec<40>();
   if (warp == C::kLoadWarp || warp == C::kLoad2Warp) {
     // ------------------- a3: producers (weights | tokens + scales) ----
     // two warps: each TMA / bulk-copy issue costs the issuing thread ~10^2
     // cycles, and one thread issuing all of a block's copies was the rate limit
     const bool wrole = warp == C::kLoadWarp;
-    // PDL: the token producer waits for the preceding quantizer before its
-    // first load; the weight producer first warms L2 with its first blocks
-    // (cannot expose stale data), then waits too (the weights may have been
-    // written by the predecessor)
+    // PDL: both producers wait for the preceding kernel before their first
+    // load (the planes, scales and possibly the weights come from it); the
+    // prologue above (barrier init, TMEM allocation, descriptor prefetch)
+    // already overlapped it.  (An L2 prefetch of the first weight blocks
+    // before the wait, as in the decode kernel, measured slower here.)
     int pg = 0, pt = cluster, pb = 0, pm0 = 0, pn0 = 0;
     sched.coords(pt, pm0, pn0);
-    if (wrole && elect_one() && pt < sched.tiles) {
-      const int R = pn0 + C::kRows * (int)crank;
-      const int v = max(0, min(C::kRows, args.N - R));
-      for (int b = 0; b < min(nb, C::kLStages + C::kStages); ++b)
-        for (int r = R, left = v; left > 0;) {
-          const int in_slab = min(left, 128 - (r & 127));
-          bulk_prefetch_l2(args.Wq + ((int64_t)(r >> 7) * nb + b) * 8192 + (r & 127) * 64, in_slab * 64);
-          r += in_slab;
-          left -= in_slab;
-        }
-    }
     __syncwarp();
     grid_dep_wait();
     for (; pg < steps;) {
@@ -325,7 +326,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
       }
       __syncwarp();
     }
-  } else if (warp >= 12 && warp < 16) {
+  }  // warp 19: idle
+  } else if (warp >= 12) {
+    if (COMET_PF_REGS) setmaxnreg_dec<64>();
     // ---- warps 12-15: a4 staging (thread = token row of lane quarter q) ----
     const int q = warp & 3;
     const int et = threadIdx.x - 384;  // 0..127
@@ -407,7 +410,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
       if (lane == 0) mbar_arrive_cluster(leader_ready + s * 8);
       trace(tr_cta && threadIdx.x == 384, 1, j);
     }
-  } else if (warp < 12) {
+  } else {
+    if (COMET_PF_REGS) setmaxnreg_inc<120>();
     // ------------------------ warps 0-11: a6 promotion + a8 write-back ----
     const int q = warp & 3;         // TMEM lane quarter
     const int kw = warp >> 2;       // 0..2: item columns [kWCols kw, kWCols (kw + 1)) of every item
@@ -496,6 +500,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
             }
           };
           constexpr int kC = kWC / 8;
+          if (COMET_PF_REGS) {
+            // setmaxnreg gave this warpgroup 120 registers: 7 of the 8 chunks
+            // are loaded at once, the 8th into the first chunk's registers
+            // after its promotion, and the accumulator is released right
+            // after -- its hold time is the load stream plus one chunk of math
+            uint32_t rq[7][8];
+#pragma unroll
+            for (int c = 0; c < 7; ++c) tmem_ld_32x32b_x8(ta + 8 * c, rq[c]);
+#pragma unroll
+            for (int c = 0; c < 7; ++c) tmem_ld_wait_dep(rq[c]);
+            promote8(0, rq[0]);
+            tmem_ld_32x32b_x8(ta + 56, rq[0]);
+            tmem_ld_wait_dep(rq[0]);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(leader_tempty + acc * 8);
+#pragma unroll
+            for (int c = 1; c < 7; ++c) promote8(c, rq[c]);
+            promote8(7, rq[0]);
+          } else {
           uint32_t ra[8], rb[8];
           tmem_ld_32x32b_x8(ta, ra);
           tmem_ld_wait_dep(ra);
@@ -513,6 +537,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
             }
             promote8(c + 1, rb);
             if (c + 2 < kC) tmem_ld_wait_dep(ra);
+          }
           }
         } else {
           // 16 columns per tcgen05.ld (the running sums leave room for 16);
