@@ -99,6 +99,20 @@ def test_ragged_m_all_tile_widths(M, group):
     assert_y_close(g["Y"], o["y"], o["y64"])
 
 
+@pytest.mark.parametrize("N", [128, 256, 512, 640, 768])
+@pytest.mark.parametrize("group", [128, 1024])
+def test_prefill_pair_tile_edges(N, group):
+    """Prefill pair tiles are 192 weight channels (96 per CTA): N % 192 in
+    {0, 64, 128} gives tiles whose second CTA holds a partial slab (v < 96),
+    straddles a 128-row slab of the tiled weight layout, or has no rows."""
+    p = synth.make_problem(300, N, 1024, n8=2, seed=500 + N, mask="scattered")
+    g = gpu_path(p, group, want_acc=True)
+    o = oracle_path(p, group, want_acc=True)
+    assert_planes_equal(g, o)
+    assert np.array_equal(g["Acc"], o["acc"])
+    assert_y_close(g["Y"], o["y"], o["y64"])
+
+
 @pytest.mark.parametrize("M,N,K", [(1, 4096, 4096), (16, 1024, 4096), (8, 512, 8192), (128, 256, 2048)])
 def test_split_k_decode_shapes(M, N, K):
     """Few tiles -> split-K with the deterministic last-CTA fixup (a7)."""
