@@ -450,6 +450,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
       const uint32_t slot = scale_base + a * C::kSlotBytes;
       const bool is8 = (map.code[b] >> 15) != 0;
       const float sxv = sx_next;
+      // next block's scale, issued now: its barrier wait and shared load
+      // overlap this block's promotion instead of following it
+      sx_next = fetch_sx(g + 1, b + 1 == nb ? 0 : b + 1);
       trace(tr_cta && threadIdx.x == 0, 11, g);
       const uint64_t sx2 = pack2(sxv, sxv);
 #pragma unroll
@@ -600,7 +603,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
           if (lane == 0) mbar_arrive_cluster(leader_tempty + acc * 8);
         }
         trace(tr_cta && threadIdx.x == 0, 3 + 2 * h, g);
-        if (h == 0) sx_next = fetch_sx(g + 1, b + 1 == nb ? 0 : b + 1);
       }
 
       if (++b == nb) {
