@@ -696,8 +696,8 @@ int comet_debug_cta_times(int enable, unsigned long long* host, int n) {
 int comet_debug_role_cycles(unsigned long long* host16) {
   return cudaMemcpyFromSymbol(host16, g_role_cycles, sizeof(unsigned long long) * 16) == cudaSuccess ? 0 : -1;
 }
-int comet_debug_trace(unsigned long long* host768) {
-  return cudaMemcpyFromSymbol(host768, g_trace, sizeof(unsigned long long) * 768) == cudaSuccess ? 0 : -1;
+int comet_debug_trace(unsigned long long* host1280) {  // 20 x 64 entries
+  return cudaMemcpyFromSymbol(host1280, g_trace, sizeof(unsigned long long) * 1280) == cudaSuccess ? 0 : -1;
 }
 int64_t comet_launch_count(void) { return g_launches.load(); }
 

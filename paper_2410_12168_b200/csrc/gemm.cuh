@@ -82,7 +82,7 @@ struct RoleTimer {
 // (0 W issue, 1 X issue, 2 data arrived, 3 expanded, 4 MMA issued,
 //  5 accumulator ready, 6 accumulator released, 7 unit retired,
 //  8 epilogue iteration top, 9 epilogue scales ready)
-__device__ unsigned long long g_trace[12][64];
+__device__ unsigned long long g_trace[20][64];
 DEVI void trace(bool on, int ev, int i) {
   if (kTraceBuild && on && i < 64) g_trace[ev][i] = clk64();
 }

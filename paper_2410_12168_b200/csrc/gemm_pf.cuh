@@ -72,19 +72,40 @@ template <int kSleep>
 DEVI void pf_wait(uint64_t* bar, uint32_t parity) {
   if (kSleep) mbar_wait_sleep(bar, parity); else mbar_wait(bar, parity);
 }
+#ifndef COMET_PF_CLUSTER_ACQ
+#define COMET_PF_CLUSTER_ACQ 0
+#endif
+// the MMA issuer's waits on barriers the partner CTA arrives on remotely.
+// acquire.cta suffices: what they publish is read by the tensor core (smem
+// operands after fence.proxy.async, TMEM after tcgen05.fence), not by generic
+// loads; an acquire.cluster wait compiles to an L1 invalidation (CCTL.IVALL)
+// per completed wait, on the MMA issue path
 template <int kSleep>
 DEVI void pf_wait_cluster(uint64_t* bar, uint32_t parity) {
-  if (kSleep) mbar_wait_cluster_sleep(bar, parity); else mbar_wait_cluster(bar, parity);
+  if (COMET_PF_CLUSTER_ACQ) {
+    if (kSleep) mbar_wait_cluster_sleep(bar, parity); else mbar_wait_cluster(bar, parity);
+  } else {
+    if (kSleep) mbar_wait_sleep(bar, parity); else mbar_wait(bar, parity);
+  }
 }
 
 #ifndef COMET_PF_EXP
 #define COMET_PF_EXP 0  // timing experiments only (wrong results): 1 = skip staging work, 2 = skip promotion math, 3 = both, 4 = also skip the accumulator loads, 5 = also skip the operand loads
 #endif
 
+#ifndef COMET_PF_NOSX
+#define COMET_PF_NOSX 0  // timing experiment: skip the activation-scale loads (wrong results)
+#endif
 #ifndef COMET_PF_REGS
 #define COMET_PF_REGS 0  // 1: setmaxnreg rebalancing (promotion 120 / staging 64 / producers+MMA 40); ptxas
                          // still pipelines the accumulator loads 3 deep, so no gain -- and the pool is the
                          // launch allocation (96 x 640), not 64K: a larger inc deadlocks
+#endif
+#ifndef COMET_PF_SXCHAIN
+#define COMET_PF_SXCHAIN 1  // scales complete on the load-ring barrier (no scale barrier wait in the promotion)
+#endif
+#ifndef COMET_PF_STPIPE
+#define COMET_PF_STPIPE 0  // 1: staging warps prefetch the next block's shared-memory operands (measured 9% slower)
 #endif
 #ifndef COMET_PF_LDPIPE
 #define COMET_PF_LDPIPE 1  // double-buffered 8-column accumulator loads in the promotion
@@ -98,7 +119,12 @@ struct PfCfg {
 #endif
   static constexpr int kItems = COMET_PF_ITEMS;  // MMA items per block (1: N=192; 2: N=96 halves)
   static constexpr int kItemN = kTileN / kItems;  // MMA N of one item (kItemN/2 rows from each CTA)
-  static constexpr int kWCols = kItemN / 3;       // item columns per promotion warp (3 per lane quarter)
+#ifndef COMET_PF_PQ
+#define COMET_PF_PQ 3  // measured: 2 (16 warps) -7%, 4 (24 warps, 80 regs) -12%, 6 -22%
+#endif
+  static constexpr int kPQ = COMET_PF_PQ;         // promotion warps per TMEM lane quarter
+  static constexpr int kPWarps = 4 * kPQ;         // promotion warps (0 .. kPWarps - 1)
+  static constexpr int kWCols = kItemN / kPQ;     // item columns per promotion warp
 #ifndef COMET_PF_LSTAGES
 #define COMET_PF_LSTAGES 5
 #endif
@@ -119,21 +145,47 @@ struct PfCfg {
   static constexpr int kSlotBytes = kSwOff + kTileN * 4;
   static constexpr int kYBoxBytes = 32 * 16 * 2;                 // 32 rows x 16 fp16
   static constexpr int kYBase = kScaleBase + kScaleSlots * kSlotBytes;
-  static constexpr int kBarBase = kYBase + 12 * 4 * kYBoxBytes;  // 12 promotion warps x 4 boxes
+  static constexpr int kYBoxes = kItems * kWCols / 16;           // 32 x 16 output boxes per promotion warp
+  static constexpr int kBarBase = kYBase + kPWarps * kYBoxes * kYBoxBytes;
   static constexpr int kBarBytes = 512;
-  static constexpr int kSmemBytes = kBarBase + kBarBytes + 1024;
+  static constexpr int kFacBase = kBarBase + kBarBytes;  // float fac[nb]: 1/16 (INT8 block) or 1/256 (INT4)
+  static constexpr int kSmemBytes = kFacBase + 512 * 4 + 1024;
   static_assert(kWEBytes % 1024 == 0 && kXBase % 1024 == 0 && kWPBase % 512 == 0, "operand alignment");
   static_assert(kScaleBase % 16 == 0 && kYBase % 128 == 0, "alignment");
   static_assert(kSmemBytes <= 227 * 1024, "smem budget");
   static constexpr int kAccCols = kItemN;
   static constexpr int kAOff = kAccs * kAccCols;  // TMEM A slots after the accumulators
   static_assert(kAOff + 32 * kStages <= 512, "TMEM budget");
-  static constexpr int kThreads = 640;
-  static constexpr int kLoadWarp = 16;   // weights
-  static constexpr int kMmaWarp = 17;
-  static constexpr int kLoad2Warp = 18;  // tokens + scales (warp 19 idle)
-  static constexpr int kReadyCount = 2 * 4;         // both CTAs' staging warps
-  static constexpr int kTemptyCount = 2 * 12;       // both CTAs' promotion warps
+#ifndef COMET_PF_ROLES_FIRST
+#define COMET_PF_ROLES_FIRST 1  // measured neutral (+-0.5%)
+#endif
+  // warp order = scheduling priority among the warps of an SMSP (lower ids
+  // win when several are ready): the latency-critical role warps (producers,
+  // MMA issuer) and the staging warps first, the promotion warps last
+#ifndef COMET_PF_STAGE6
+#define COMET_PF_STAGE6 0  // measured -6% (21 warps round to 24: 80 registers)
+#endif
+  // STAGE6 (roles first only): 6 staging warps -- warps 4..7 expand tokens
+  // into TMEM (one per lane quarter), warps 3 and 8 expand weights into smem --
+  // instead of 4 doing both; 3 role warps (no idle warp), promotion warps 9..20:
+  // 21 warps still leave 96 registers per thread
+  static constexpr bool kStage6 = COMET_PF_STAGE6 && COMET_PF_ROLES_FIRST;
+  static constexpr int kStageWarps = kStage6 ? 6 : 4;
+  static constexpr int kRoleWarps = kStage6 ? 3 : 4;
+  static constexpr int kRoleBase = COMET_PF_ROLES_FIRST ? 0 : kPWarps + kStageWarps;  // role warps
+  static constexpr int kStageWarp = COMET_PF_ROLES_FIRST ? kRoleWarps : kPWarps;    // staging warps
+  static constexpr int kTokWarp = kStage6 ? 4 : kStageWarp;                          // first token warp
+  static constexpr int kPBase = COMET_PF_ROLES_FIRST ? kRoleWarps + kStageWarps : 0;  // promotion warps
+  static constexpr int kWThreads = kStage6 ? 64 : 128;                               // weight-expanding threads
+  static constexpr int kLoadWarp = kRoleBase;        // weights
+  static constexpr int kMmaWarp = kRoleBase + 1;
+#ifndef COMET_PF_XWARP
+#define COMET_PF_XWARP 6  // 7: token producer on the 4th SMSP (measured neutral)
+#endif
+  static constexpr int kLoad2Warp = kRoleBase + COMET_PF_XWARP - 4;  // tokens + scales (the 4th warp idles)
+  static constexpr int kThreads = 32 * (kPWarps + kRoleWarps + kStageWarps);
+  static constexpr int kReadyCount = 2 * kStageWarps;  // both CTAs' staging warps
+  static constexpr int kTemptyCount = 2 * kPWarps;   // both CTAs' promotion warps
 };
 
 struct PfSched {
@@ -154,7 +206,7 @@ __host__ __device__ constexpr int pf_col(int h, int j) {
 }
 
 template <bool kGroupK, bool kAccOut>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
     w4ax_gemm_pf_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmX4,
                         const __grid_constant__ CUtensorMap tmX8, const __grid_constant__ BlockMap map, GemmArgs args,
                         PfSched sched) {
@@ -192,7 +244,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
     }
     for (int l = 0; l < C::kLStages; ++l) {
       mbar_init(&lfull[l], 2);  // two producers
-      mbar_init(&lempty[l], 4);
+      mbar_init(&lempty[l], C::kStageWarps);
     }
     for (int a = 0; a < C::kAccs; ++a) {
       mbar_init(&tfull[a], 1);
@@ -200,10 +252,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
     }
     for (int a = 0; a < C::kScaleSlots; ++a) {
       mbar_init(&sfull[a], 1);
-      mbar_init(&sempty[a], 12);
+      mbar_init(&sempty[a], C::kPWarps);
     }
     fence_mbar_init();
   }
+  // per-block activation-scale factor (the x16 / x256 of the expanded operands)
+  for (int i = threadIdx.x; i < nb; i += C::kThreads)
+    reinterpret_cast<float*>(smem + C::kFacBase)[i] = (map.code[i] >> 15) ? 0.0625f : 0.00390625f;
   if (warp == C::kLoadWarp && lane == 0) {
     if (!kAccOut) tma_prefetch_desc(&tmY);
     tma_prefetch_desc(&tmX4);
@@ -216,12 +271,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
   const uint32_t tmem_base = *tmem_holder;
   // debug trace of one CTA (COMET_TRACE builds; tools/gemm_sweep.py trace3)
   const bool tr_cta = kTraceBuild && g_cta_times_on && blockIdx.x + 1 == g_cta_times_on;
+  const bool tr_pair = kTraceBuild && g_cta_times_on && (blockIdx.x >> 1) == ((g_cta_times_on - 1) >> 1);
 
   // register rebalancing per warpgroup (the launch pool 96 x 640 = 3 x 128 x 120
   // + 128 x 64 + 128 x 40 + slack; every warp of a warpgroup executes the same setmaxnreg, inside
   // the warpgroup's branch so ptxas allocates each role's code to its budget):
   // the promotion warps hold the running sums (64) and 7 accumulator chunks
-  if (warp >= 16) {
+  if (warp >= C::kRoleBase && warp < C::kRoleBase + C::kRoleWarps) {
   if (COMET_PF_REGS) setmaxnreg_dec<40>();
   if (warp == C::kLoadWarp || warp == C::kLoad2Warp) {
     // ------------------- a3: producers (weights | tokens + scales) ----
@@ -247,6 +303,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
       // (the producer, MMA and staging warps run ahead of the promotion: their
       // waits suspend instead of polling, leaving issue slots to the promotion)
       pf_wait<COMET_PF_SLEEP & 1>(&lempty[l], ((g / C::kLStages) & 1) ^ 1);
+      if (elect_one()) trace(tr_cta, wrole ? 14 : 15, g);
       if (!kAccOut && !wrole) pf_wait<COMET_PF_SLEEP & 1>(&sempty[a], ((g / C::kScaleSlots) & 1) ^ 1);
       const uint32_t code = map.code[b];
       const bool is8 = (code >> 15) != 0;
@@ -270,7 +327,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
             left -= in_slab;
           }
         } else {
-          mbar_arrive_expect_tx(&lfull[l], COMET_PF_EXP >= 5 ? 0 : (is8 ? 128 * 128 : 128 * 64));
+          const int nsx = kAccOut ? 0 : max(0, min(128, (int)args.ldsx - my_m0));  // multiple of 4
+          const bool load_sw = !kGroupK || b == nb - 1;
+          const int nsw = (kAccOut || !load_sw) ? 0 : max(0, min(C::kTileN, args.N - pn0));  // multiple of 64
+          // COMET_PF_SXCHAIN: the scales complete on the load-ring barrier with
+          // the tokens; the promotion reads them after the block's tfull, which
+          // follows lfull through staging -> ready -> MMA -> commit
+          mbar_arrive_expect_tx(&lfull[l], (COMET_PF_EXP >= 5 ? 0 : (is8 ? 128 * 128 : 128 * 64)) +
+                                               (COMET_PF_SXCHAIN ? ((COMET_PF_NOSX ? 0 : nsx) + nsw) * 4 : 0));
           uint8_t* xs = smem + C::kXBase + l * C::kXStageBytes;
           if (COMET_PF_EXP >= 5) {  // 5: no operand loads, 6: no token loads
           } else if (is8)
@@ -278,14 +342,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
           else
             tma_load_2d(xs, &tmX4, &lfull[l], rank * 64, my_m0);
           if (!kAccOut) {
-            const int nsx = max(0, min(128, (int)args.ldsx - my_m0));  // multiple of 4
-            const bool load_sw = !kGroupK || b == nb - 1;
-            const int nsw = load_sw ? max(0, min(C::kTileN, args.N - pn0)) : 0;  // multiple of 64
-            mbar_arrive_expect_tx(&sfull[a], (nsx + nsw) * 4);
+            uint64_t* sb = COMET_PF_SXCHAIN ? &lfull[l] : &sfull[a];
+            if (!COMET_PF_SXCHAIN) mbar_arrive_expect_tx(&sfull[a], (nsx + nsw) * 4);
             uint8_t* slot = smem + C::kScaleBase + a * C::kSlotBytes;
-            if (nsx) bulk_load(slot, args.Sx + (int64_t)b * args.ldsx + my_m0, nsx * 4, &sfull[a]);
-            if (nsw)
-              bulk_load(slot + C::kSwOff, args.Sw + (kGroupK ? 0 : (int64_t)b * args.N) + pn0, nsw * 4, &sfull[a]);
+            if (nsx && !COMET_PF_NOSX) bulk_load(slot, args.Sx + (int64_t)b * args.ldsx + my_m0, nsx * 4, sb);
+            if (nsw) bulk_load(slot + C::kSwOff, args.Sw + (kGroupK ? 0 : (int64_t)b * args.N) + pn0, nsw * 4, sb);
           }
         }
         trace(!kTraceEv2 && tr_cta, 9, g);
@@ -308,18 +369,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
       const int g = i / C::kItems, h = i % C::kItems;
       const int s = g % C::kStages, acc = i % C::kAccs;
       if (h == 0) pf_wait_cluster<COMET_PF_SLEEP & 2>(&ready[s], (g / C::kStages) & 1);
+      if (!kTraceEv2 && C::kItems == 1 && elect_one()) trace(tr_cta, 6, g);
       // magic mode: use k of an accumulator waits for its k-th refill (the
       // promotion warps' initial fill is completion 0)
       pf_wait_cluster<COMET_PF_SLEEP & 2>(&tempty[acc], ((i / C::kAccs) & 1) ^ (kPfMagic ? 0 : 1));
+      if (C::kItems == 1 && elect_one()) trace(tr_cta, 8, g);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t a_tm = tmem_base + C::kAOff + 32 * s;
         const uint32_t bst = sbase + s * C::kWEBytes;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < 4; ++k) {
           mma_i8_ts_2sm(tmem_base + acc * C::kAccCols, a_tm + 8 * k,
                         umma_desc_sw128_kmajor(bst + h * (C::kRows / C::kItems) * 128 + 32 * k), idesc,
                         (kPfMagic || k > 0) ? 1u : 0u);
+          if (k == 0 && g < 32) trace(tr_cta, 4, 32 + g);
+        }
+        if (g < 32) trace(tr_cta, 5, 32 + g);
         mma_commit_2sm(&tfull[acc], 0x3);
         if (h == C::kItems - 1) mma_commit_2sm(&mdone[s], 0x3);
         trace(tr_cta, 7 + h, g);
@@ -327,13 +393,108 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
       __syncwarp();
     }
   }  // warp 19: idle
-  } else if (warp >= 12) {
+  } else if (warp >= C::kStageWarp && warp < C::kStageWarp + C::kStageWarps) {
     if (COMET_PF_REGS) setmaxnreg_dec<64>();
+    const bool do_tok = !C::kStage6 || (warp >= C::kTokWarp && warp < C::kTokWarp + 4);
+    const bool do_w = !C::kStage6 || !do_tok;
     // ---- warps 12-15: a4 staging (thread = token row of lane quarter q) ----
     const int q = warp & 3;
-    const int et = threadIdx.x - 384;  // 0..127
+    // weight-expanding thread index 0 .. kWThreads-1
+    const int et = C::kStage6 ? lane + (warp == C::kStageWarp ? 0 : 32) : (int)threadIdx.x - 32 * C::kStageWarp;
     const uint32_t tst = tmem_base + ((uint32_t)(32 * q) << 16) + C::kAOff;
     const uint32_t leader_ready = mapa_shared(smem_u32(ready), 0);
+    if (COMET_PF_STPIPE && COMET_PF_EXP == 0) {
+      // software-pipelined: the shared-memory loads of block j + 1 are issued
+      // right after block j's operands are written, so their latency overlaps
+      // block j's hand-off (fence, TMEM-store wait, ready arrive) and the next
+      // block's barrier waits instead of following them
+      constexpr int kWC4 = C::kRows * 4 / C::kWThreads;
+      const uint32_t r_ = (32 * q) + (opaque(threadIdx.x) & 31);  // this thread's token row
+      auto load_block = [&](int jj, bool is8j, uint4(&tv)[8], uint4(&wv)[kWC4]) {
+        const int l = jj % C::kLStages;
+        const uint32_t xs = sbase + C::kXBase + l * C::kXStageBytes;
+        const uint32_t wps = sbase + C::kWPBase + l * C::kWPBytes;
+        pf_wait<COMET_PF_SLEEP & 4>(&lfull[l], (jj / C::kLStages) & 1);
+        if (!do_tok) {
+        } else if (is8j) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) tv[c] = lds128(xs + r_ * 128 + ((c ^ (r_ & 7)) << 4));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tv[c] = lds128(xs + r_ * 64 + ((c ^ ((r_ >> 1) & 3)) << 4));
+        }
+#pragma unroll
+        for (int k = 0; k < kWC4 && do_w; ++k) {
+          const int ch = et + C::kWThreads * k;
+          const int er = ch >> 2, ej = ch & 3;
+          wv[k] = lds128(wps + er * 64 + ((ej ^ ((er >> 1) & 3)) << 4));
+        }
+      };
+      auto stage_block = [&](int jj, bool is8j, uint4(&tv)[8], uint4(&wv)[kWC4], bool is8n,
+                             uint4(&tvn)[8], uint4(&wvn)[kWC4]) {
+        const int l = jj % C::kLStages, s = jj % C::kStages;
+        const uint32_t wst = sbase + s * C::kWEBytes;
+        // operand stage s (smem B + TMEM A slot) is free once the MMAs of
+        // block jj - kStages are done
+        pf_wait<COMET_PF_SLEEP & 4>(&mdone[s], ((jj / C::kStages) & 1) ^ 1);
+        trace(tr_cta && threadIdx.x == 32 * C::kTokWarp, 10, jj);
+        tc_fence_after();
+        if (do_tok) {  // tokens: 4 chunks of 32 K = 32 TMEM A columns (INT8 raw, INT4 x16)
+          uint32_t e[32];
+          if (is8j) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              e[4 * c] = tv[c].x; e[4 * c + 1] = tv[c].y; e[4 * c + 2] = tv[c].z; e[4 * c + 3] = tv[c].w;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              zext_word(tv[c].x, e[8 * c + 0], e[8 * c + 1]);
+              zext_word(tv[c].y, e[8 * c + 2], e[8 * c + 3]);
+              zext_word(tv[c].z, e[8 * c + 4], e[8 * c + 5]);
+              zext_word(tv[c].w, e[8 * c + 6], e[8 * c + 7]);
+            }
+          }
+          tmem_st_32x32b_x32(tst + 32 * s, e);
+        }
+#pragma unroll
+        for (int k = 0; k < kWC4 && do_w; ++k) {  // weights -> SW128 B operand
+          const int ch = et + C::kWThreads * k;
+          const int er = ch >> 2, ej = ch & 3;
+          expand_chunk(wv[k], wst + er * 128 + (((2 * ej) ^ (er & 7)) << 4),
+                       wst + er * 128 + (((2 * ej + 1) ^ (er & 7)) << 4));
+        }
+        // the load stage may be refilled once every lane's loads have been
+        // consumed (by the tcgen05.st / st.shared above)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&lempty[l]);
+        fence_proxy_async_smem();
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_ready + s * 8);
+        trace(tr_cta && threadIdx.x == 32 * C::kTokWarp, 1, jj);
+        // (after the fence: a proxy fence waits for the warp's outstanding
+        // shared-memory loads)
+        if (jj + 1 < steps) load_block(jj + 1, is8n, tvn, wvn);
+      };
+      int sb = 0;
+      auto next_is8 = [&]() {
+        const bool r = (map.code[sb] >> 15) != 0;
+        if (++sb == nb) sb = 0;
+        return r;
+      };
+      // one register set: block j's operands are consumed before block j + 1's
+      // loads are issued into the same registers
+      uint4 tv[8], wv[kWC4];
+      bool is8 = next_is8();
+      if (steps > 0) load_block(0, is8, tv, wv);
+      for (int j = 0; j < steps; ++j) {
+        const bool is8n = next_is8();  // block j + 1
+        stage_block(j, is8, tv, wv, is8n, tv, wv);
+        is8 = is8n;
+      }
+    } else {
     int sb = 0;
     for (int j = 0; j < steps; ++j) {
       // ---- a4: stage block j: load stage l -> operand stage s ----
@@ -344,10 +505,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
       const uint32_t wps = sbase + C::kWPBase + l * C::kWPBytes;
       const uint32_t wst = sbase + s * C::kWEBytes;
       pf_wait<COMET_PF_SLEEP & 4>(&lfull[l], (j / C::kLStages) & 1);
+      trace(tr_cta && threadIdx.x == 32 * C::kTokWarp, 12, j);
       // operand stage s (smem B + TMEM A slot) is free once the MMAs of block
       // j - kStages are done
       pf_wait<COMET_PF_SLEEP & 4>(&mdone[s], ((j / C::kStages) & 1) ^ 1);
-      trace(tr_cta && threadIdx.x == 384, 10, j);
+      trace(tr_cta && threadIdx.x == 32 * C::kTokWarp, 10, j);
       tc_fence_after();
       if (COMET_PF_EXP != 1 && COMET_PF_EXP < 3) {
       // all shared-memory loads of the block first (the loads and stores are
@@ -355,22 +517,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
       // one load latency per chunk)
       const uint32_t r_ = (32 * q) + (opaque(threadIdx.x) & 31);  // this thread's token row
       uint4 tv[8];
-      if (is8) {
+      if (!do_tok) {
+      } else if (is8) {
 #pragma unroll
         for (int c = 0; c < 8; ++c) tv[c] = lds128(xs + r_ * 128 + ((c ^ (r_ & 7)) << 4));
       } else {
 #pragma unroll
         for (int c = 0; c < 4; ++c) tv[c] = lds128(xs + r_ * 64 + ((c ^ ((r_ >> 1) & 3)) << 4));
       }
-      uint4 wv[C::kRows * 4 / 128];
+      uint4 wv[C::kRows * 4 / C::kWThreads];
 #pragma unroll
-      for (int k = 0; k < C::kRows * 4 / 128; ++k) {
-        const int ch = et + 128 * k;
+      for (int k = 0; k < C::kRows * 4 / C::kWThreads && do_w; ++k) {
+        const int ch = et + C::kWThreads * k;
         const int er = ch >> 2, ej = ch & 3;
         wv[k] = lds128(wps + er * 64 + ((ej ^ ((er >> 1) & 3)) << 4));
       }
+      if (kTraceBuild) {  // the LDS results have landed
+        uint32_t dep = tv[0].x ^ tv[3].w;
+        if (do_w) dep ^= wv[0].x ^ wv[C::kRows * 4 / C::kWThreads - 1].w;
+        trace(tr_cta && threadIdx.x == 32 * C::kTokWarp && dep != 0x9e3779b9u, 16, j);
+      }
       // tokens: 4 chunks of 32 K = 32 TMEM A columns (INT8 raw, INT4 x16)
-      {
+      if (do_tok) {
         uint32_t e[32];
         if (is8) {
 #pragma unroll
@@ -386,13 +554,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
             zext_word(tv[c].w, e[8 * c + 6], e[8 * c + 7]);
           }
         }
+        if (kTraceBuild) {  // after the zero-extension (its inputs: the LDS results)
+          uint32_t dep = 0;
+#pragma unroll
+          for (int x = 0; x < 32; ++x) dep ^= e[x];
+          trace(tr_cta && threadIdx.x == 32 * C::kTokWarp && dep != 0x9e3779b9u, 13, j);
+        }
         tmem_st_32x32b_x32(tst + 32 * s, e);
       }
-      trace(kTraceEv2 && tr_cta && threadIdx.x == 384, 6, j);
+      trace(kTraceEv2 && tr_cta && threadIdx.x == 32 * C::kTokWarp, 6, j);
       // weights: chunks et, et + 128, et + 256 of the packed slab -> SW128 B operand
 #pragma unroll
-      for (int k = 0; k < C::kRows * 4 / 128; ++k) {
-        const int ch = et + 128 * k;
+      for (int k = 0; k < C::kRows * 4 / C::kWThreads && do_w; ++k) {
+        const int ch = et + C::kWThreads * k;
         const int er = ch >> 2, ej = ch & 3;
         expand_chunk(wv[k], wst + er * 128 + (((2 * ej) ^ (er & 7)) << 4), wst + er * 128 + (((2 * ej + 1) ^ (er & 7)) << 4));
       }
@@ -402,32 +576,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
       // the LDS instructions could overtake them)
       __syncwarp();
       if (lane == 0) mbar_arrive(&lempty[l]);
-      trace(kTraceEv2 && tr_cta && threadIdx.x == 384, 9, j);
+      trace(kTraceEv2 && tr_cta && threadIdx.x == 32 * C::kTokWarp, 9, j);
       fence_proxy_async_smem();
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_ready + s * 8);
-      trace(tr_cta && threadIdx.x == 384, 1, j);
+      trace(tr_cta && threadIdx.x == 32 * C::kTokWarp, 1, j);
+    }
     }
   } else {
     if (COMET_PF_REGS) setmaxnreg_inc<120>();
+
     // ------------------------ warps 0-11: a6 promotion + a8 write-back ----
     const int q = warp & 3;         // TMEM lane quarter
-    const int kw = warp >> 2;       // 0..2: item columns [kWCols kw, kWCols (kw + 1)) of every item
+    const int kw = (warp - C::kPBase) >> 2;  // 0..kPQ-1: item columns [kWCols kw, kWCols (kw + 1)) of every item
     const int row = 32 * q + lane;  // token row within this CTA
     const uint32_t tl = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(C::kWCols * kw);
     const uint32_t leader_tempty = mapa_shared(smem_u32(tempty), 0);
 
     constexpr int kWC = C::kWCols;  // this warp's columns of an item
-    uint64_t y[32];  // [item h][kWC / 2 pairs]: columns kWC kw + 2p (+1) of item h
+    uint64_t y[C::kItems * kWC / 2];  // [item h][kWC / 2 pairs]: columns kWC kw + 2p (+1) of item h
 #pragma unroll
-    for (int j = 0; j < 32; ++j) y[j] = 0;
+    for (int j = 0; j < C::kItems * kWC / 2; ++j) y[j] = 0;
     int t = cluster, b = 0;
     // this row's activation scale of block g (x 16^-e_g), fetched one block
     // ahead so its barrier wait and load latency overlap the promotion
     auto fetch_sx = [&](int g, int bb) -> float {
-      if (kAccOut || g >= steps) return 0.f;
+      if (kAccOut || COMET_PF_SXCHAIN || g >= steps) return 0.f;
       const int a = g & (C::kScaleSlots - 1);
       mbar_wait(&sfull[a], (g / C::kScaleSlots) & 1);
       const bool is8 = (map.code[bb] >> 15) != 0;
@@ -445,23 +621,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
         for (int acc = 0; acc < C::kAccs; ++acc) mbar_arrive_cluster(leader_tempty + acc * 8);
     }
     for (int g = 0; g < steps; ++g) {
-      trace(tr_cta && threadIdx.x == 0, 0, g);
+      trace(tr_cta && threadIdx.x == 32 * C::kPBase, 0, g);
       const int a = g & (C::kScaleSlots - 1);
       const uint32_t slot = scale_base + a * C::kSlotBytes;
       const bool is8 = (map.code[b] >> 15) != 0;
-      const float sxv = sx_next;
-      // next block's scale, issued now: its barrier wait and shared load
-      // overlap this block's promotion instead of following it
-      sx_next = fetch_sx(g + 1, b + 1 == nb ? 0 : b + 1);
-      trace(tr_cta && threadIdx.x == 0, 11, g);
-      const uint64_t sx2 = pack2(sxv, sxv);
+      // (without COMET_PF_SXCHAIN) next block's scale, issued now: its barrier
+      // wait and shared load overlap this block's promotion
+      uint64_t sx2 = pack2(sx_next, sx_next);
+      if (!COMET_PF_SXCHAIN) sx_next = fetch_sx(g + 1, b + 1 == nb ? 0 : b + 1);
+      trace(tr_cta && threadIdx.x == 32 * C::kPBase, 11, g);
 #pragma unroll
       for (int h = 0; h < C::kItems; ++h) {
         const int i = C::kItems * g + h;
         const int acc = i % C::kAccs;
-        mbar_wait(&tfull[acc], (i / C::kAccs) & 1);
-        trace(tr_cta && threadIdx.x == 0, 2 + 2 * h, g);
+        pf_wait<COMET_PF_SLEEP & 8>(&tfull[acc], (i / C::kAccs) & 1);
+        trace(tr_cta && threadIdx.x == 32 * C::kPBase, 2 + 2 * h, g);
         tc_fence_after();
+        if (COMET_PF_SXCHAIN && !kAccOut && h == 0) {
+          const float sxv = lds_f32(slot + row * 4) * lds_f32(sbase + C::kFacBase + 4 * b);
+          sx2 = pack2(sxv, sxv);
+        }
         const uint32_t ta = tl + acc * C::kAccCols;
         if (kAccOut) {
           int m0, n0;
@@ -537,6 +716,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive_cluster(leader_tempty + acc * 8);
+              // per-warp release times of steps 10 and 11, both CTAs of the traced pair
+              if (C::kItems == 1 && (g == 10 || g == 11)) trace(tr_pair && lane == 0, g - 6, warp - C::kPBase + 16 * (int)crank);
             }
             promote8(c + 1, rb);
             if (c + 2 < kC) tmem_ld_wait_dep(ra);
@@ -602,7 +783,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(leader_tempty + acc * 8);
         }
-        trace(tr_cta && threadIdx.x == 0, 3 + 2 * h, g);
+        trace(tr_cta && threadIdx.x == 32 * C::kPBase, 3 + 2 * h, g);
       }
 
       if (++b == nb) {
@@ -611,11 +792,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
           int m0, n0;
           sched.coords(t, m0, n0);
           const int mw = m0 + 128 * (int)crank + 32 * q;  // first row of this warp's boxes
-          const uint32_t ybuf = opaque(sbase + C::kYBase + warp * 4 * C::kYBoxBytes);
+          const uint32_t ybuf = opaque(sbase + C::kYBase + (warp - C::kPBase) * C::kYBoxes * C::kYBoxBytes);
           if (lane == 0) bulk_wait_group_read0();  // previous tile's stores have left smem
           __syncwarp();
 #pragma unroll
-          for (int bx = 0; bx < 4; ++bx) {  // box = (item h, unit u): 32 rows x 16 columns
+          for (int bx = 0; bx < C::kYBoxes; ++bx) {  // box = (item h, unit u): 32 rows x 16 columns
             const int h = bx / (kWC / 16), u = bx % (kWC / 16);
             const uint32_t swa = slot + C::kSwOff + pf_col(h, kWC * kw + 16 * u) * 4;
             uint32_t hw[8];
@@ -642,7 +823,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
           __syncwarp();
           if (lane == 0) {
 #pragma unroll
-            for (int bx = 0; bx < 4; ++bx) {
+            for (int bx = 0; bx < C::kYBoxes; ++bx) {
               const int nglob = n0 + pf_col(bx / (kWC / 16), kWC * kw + 16 * (bx % (kWC / 16)));
               if (nglob < args.N) tma_store_2d(&tmY, ybuf + bx * C::kYBoxBytes, nglob, mw);
             }
@@ -657,7 +838,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
     }
   }
 
-  if (!kAccOut && warp < 12 && lane == 0) bulk_wait_group0();  // output stores complete
+  if (!kAccOut && warp >= C::kPBase && warp < C::kPBase + C::kPWarps && lane == 0) bulk_wait_group0();  // output stores complete
   tc_fence_before();
   __syncthreads();
   cluster_sync();

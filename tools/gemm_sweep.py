@@ -157,13 +157,13 @@ def trace(M, N, K, n8, cta=0, units=24):
     L = comet.lib()
     L.comet_debug_cta_times.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
     L.comet_debug_trace.argtypes = [ctypes.c_void_p]
-    buf = (ctypes.c_ulonglong * 768)()
+    buf = (ctypes.c_ulonglong * 1280)()
     L.comet_debug_trace(buf)  # clear-less: events of untraced units stay stale, print only < units
     L.comet_debug_cta_times(cta + 1, None, 0)
     run(M, N, K, n8, "K", reps=1)
     L.comet_debug_cta_times(0, None, 0)
     L.comet_debug_trace(buf)
-    a = np.array(buf[:], dtype=np.int64).reshape(12, 64)
+    a = np.array(buf[:], dtype=np.int64).reshape(20, 64)
     t0 = a[0, 0]
     names = ["Wiss", "Xiss", "arrive", "expd", "mma", "accrdy", "accrel", "retire", "epitop", "sxrdy"]
     print(f"M={M} N={N} K={K} CTA{cta} trace (cycles rel. first W issue):")
@@ -178,18 +178,28 @@ def trace3(M, N, K, n8, cta=0, steps=40):
     L = comet.lib()
     L.comet_debug_cta_times.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
     L.comet_debug_trace.argtypes = [ctypes.c_void_p]
-    buf = (ctypes.c_ulonglong * 768)()
+    buf = (ctypes.c_ulonglong * 1280)()
     L.comet_debug_cta_times(cta + 1, None, 0)
     run(M, N, K, n8, "K", reps=1)
     L.comet_debug_cta_times(0, None, 0)
     L.comet_debug_trace(buf)
-    a = np.array(buf[:], dtype=np.int64).reshape(12, 64)
+    a = np.array(buf[:], dtype=np.int64).reshape(20, 64)
     t0 = a[0, 0]
-    names = ["Ptop", "staged", "tfull0", "prom0", "tfull1", "prom1", "ready", "mma0", "mma1", "Wiss", "Xiss", "sxrdy"]
+    names = ["Ptop", "staged", "tfull0", "prom0", "-", "-", "mrdy", "mma0", "temty", "Wiss", "Xiss", "sxrdy"]
     print(f"M={M} N={N} K={K} CTA{cta} pf trace (cycles rel. first P iteration; staged = block g+2 staged):")
     print("step " + " ".join(f"{n:>7s}" for n in names))
     for i in range(steps):
         print(f"{i:4d} " + " ".join(f"{a[e, i] - t0:7d}" for e in range(12)))
+    print("MMA issue sub-events (temty, after 1st MMA, after 4th MMA, after commits), steps 8-15:")
+    for i in range(8, 16):
+        print(f"  {i:3d} {a[8, i] - t0:7d} {a[4, 32 + i] - t0:7d} {a[5, 32 + i] - t0:7d} {a[7, i] - t0:7d}")
+    print("block: W-prod issue, X-prod issue, staging lfull seen, staging start (mdone seen), LDS landed, tokens zext done, [EV2: STTM issued, weights done], staged")
+    for i in range(8, 16):
+        print(f"  {i:3d} {a[14, i] - t0:7d} {a[15, i] - t0:7d} {a[12, i] - t0:7d} {a[10, i] - t0:7d} {a[16, i] - t0:7d} {a[13, i] - t0:7d} [{a[6, i] - t0:7d} {a[9, i] - t0:7d}] {a[1, i] - t0:7d}")
+    for e, st in ((4, 10), (5, 11)):
+        print(f"step {st} per-warp release (CTA pair, leader then partner):")
+        print("  " + " ".join(f"{a[e, w] - t0:6d}" for w in range(12)))
+        print("  " + " ".join(f"{a[e, 16 + w] - t0:6d}" for w in range(12)))
 
 
 def trace2(M, N, K, n8, cta=0, steps=40):
@@ -198,12 +208,12 @@ def trace2(M, N, K, n8, cta=0, steps=40):
     L = comet.lib()
     L.comet_debug_cta_times.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
     L.comet_debug_trace.argtypes = [ctypes.c_void_p]
-    buf = (ctypes.c_ulonglong * 768)()
+    buf = (ctypes.c_ulonglong * 1280)()
     L.comet_debug_cta_times(cta + 1, None, 0)
     run(M, N, K, n8, "K", reps=1)
     L.comet_debug_cta_times(0, None, 0)
     L.comet_debug_trace(buf)
-    a = np.array(buf[:], dtype=np.int64).reshape(12, 64)
+    a = np.array(buf[:], dtype=np.int64).reshape(20, 64)
     t0 = a[0, 0]
     names = ["iter", "fullnx", "expdnx", "sxrdy", "accrdy", "promdn", "mma", "prod"]
     print(f"M={M} N={N} K={K} CTA{cta} prefill trace (cycles rel. first iteration; fullnx/expdnx = step g):")
