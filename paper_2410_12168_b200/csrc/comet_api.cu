@@ -352,7 +352,26 @@ comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, in
   // tmW is an unused placeholder map
   if (!make_map_u8(&tmW, Wq, (uint64_t)K / 2, (uint64_t)N, (uint64_t)K / 2, 64, 128, CU_TENSOR_MAP_SWIZZLE_NONE))
     return COMET_ERR_CUDA;
-  if (n4) {
+  if (n4 && PfCfg::kXPre && p.two_sm && use_pf()) {
+    // pre-expanded INT4 token blocks (x16 INT8, staging byte order) in a
+    // cached device buffer, TMA-loaded as SW128 INT8 rows like the INT8 plane
+    static void* xe = nullptr;
+    static size_t xe_bytes = 0;
+    const size_t need = (size_t)M * n4 * 128;
+    if (need > xe_bytes) {
+      if (xe) cudaFree(xe);
+      if (cudaMalloc(&xe, need) != cudaSuccess) { xe = nullptr; xe_bytes = 0; return COMET_ERR_CUDA; }
+      xe_bytes = need;
+    }
+    const int64_t n16 = (int64_t)M * n4 * 4;
+    expand_int4_tokens_kernel<<<4 * num_sms, 256, 0, st>>>(reinterpret_cast<const uint4*>(Xq4),
+                                                           reinterpret_cast<uint4*>(xe), n16);
+    comet_status ls = check_launch();
+    if (ls != COMET_OK) return ls;
+    if (!make_map_u8(&tmX4, xe, (uint64_t)n4 * 128, (uint64_t)M, (uint64_t)n4 * 128, 128, p.bn,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+      return COMET_ERR_CUDA;
+  } else if (n4) {
     // the TMEM-A prefill kernel reads packed token rows per thread: 64B swizzle
     // keeps those 16-byte loads conflict-free
     if (!make_map_u8(&tmX4, Xq4, (uint64_t)n4 * 64, (uint64_t)M, (uint64_t)n4 * 64, 64, p.bn,

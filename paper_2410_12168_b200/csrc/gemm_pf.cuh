@@ -96,6 +96,9 @@ DEVI void pf_wait_cluster(uint64_t* bar, uint32_t parity) {
 #ifndef COMET_PF_NOSX
 #define COMET_PF_NOSX 0  // timing experiment: skip the activation-scale loads (wrong results)
 #endif
+#ifndef COMET_PF_NOLOAD
+#define COMET_PF_NOLOAD 0  // timing experiment (wrong results): 1 = no token TMA, 2 = no weight copies
+#endif
 #ifndef COMET_PF_REGS
 #define COMET_PF_REGS 0  // 1: setmaxnreg rebalancing (promotion 120 / staging 64 / producers+MMA 40); ptxas
                          // still pipelines the accumulator loads 3 deep, so no gain -- and the pool is the
@@ -103,6 +106,9 @@ DEVI void pf_wait_cluster(uint64_t* bar, uint32_t parity) {
 #endif
 #ifndef COMET_PF_SXCHAIN
 #define COMET_PF_SXCHAIN 1  // scales complete on the load-ring barrier (no scale barrier wait in the promotion)
+#endif
+#ifndef COMET_PF_XPRE
+#define COMET_PF_XPRE 0
 #endif
 #ifndef COMET_PF_STPIPE
 #define COMET_PF_STPIPE 0  // 1: staging warps prefetch the next block's shared-memory operands (measured 9% slower)
@@ -112,7 +118,10 @@ DEVI void pf_wait_cluster(uint64_t* bar, uint32_t parity) {
 #endif
 
 struct PfCfg {
-  static constexpr int kTileN = 192;          // weight rows per pair tile
+#ifndef COMET_PF_TILEN
+#define COMET_PF_TILEN 192
+#endif
+  static constexpr int kTileN = COMET_PF_TILEN;  // weight rows per pair tile
   static constexpr int kRows = kTileN / 2;    // weight rows per CTA
 #ifndef COMET_PF_ITEMS
 #define COMET_PF_ITEMS 1
@@ -133,12 +142,22 @@ struct PfCfg {
 #endif
   static constexpr int kStages = COMET_PF_STAGES;    // operand stages: SW128 B + TMEM A slot (freed by the MMA)
   static constexpr int kLStages = COMET_PF_LSTAGES;  // load stages: packed weights + raw tokens (freed by staging)
-  static constexpr int kAccs = kItems == 1 ? 2 : 4;  // kItemN-column accumulators
+#ifndef COMET_PF_ACCS
+#define COMET_PF_ACCS (COMET_PF_ITEMS == 1 ? 2 : 4)
+#endif
+  static constexpr int kAccs = COMET_PF_ACCS;  // kItemN-column accumulators
   static constexpr int kScaleSlots = 8;
   static constexpr int kWPBytes = kRows * 64;   // packed weights
   static constexpr int kWEBytes = kRows * 128;  // expanded weights, SW128 K-major
-  static constexpr int kXStageBytes = 128 * 128;  // INT8 [128 x 128] or packed INT4 [128 x 64]
-  static constexpr int kWPBase = kStages * kWEBytes;
+  // XPRE: the INT4 token blocks arrive pre-expanded to INT8 (x16, same byte
+  // order the staging warps produce) and every token block is TMA-loaded
+  // straight into a SW128 smem A stage of the operand ring (SS MMA); the
+  // staging warps then only expand weights
+  static constexpr bool kXPre = COMET_PF_XPRE;
+  static constexpr int kXStageBytes = kXPre ? 0 : 128 * 128;  // INT8 [128 x 128] or packed INT4 [128 x 64]
+  static constexpr int kAStageBytes = kXPre ? 128 * 128 : 0;  // token A operand stage (SS MMA)
+  static constexpr int kABase = kStages * kWEBytes;
+  static constexpr int kWPBase = kABase + kStages * kAStageBytes;
   static constexpr int kXBase = kWPBase + kLStages * kWPBytes;
   static constexpr int kScaleBase = kXBase + kLStages * kXStageBytes;
   static constexpr int kSwOff = 512;                             // sx[128] then sw[192]
@@ -303,6 +322,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
       // (the producer, MMA and staging warps run ahead of the promotion: their
       // waits suspend instead of polling, leaving issue slots to the promotion)
       pf_wait<COMET_PF_SLEEP & 1>(&lempty[l], ((g / C::kLStages) & 1) ^ 1);
+      // XPRE: the tokens land in operand stage g % kStages, free once the MMAs
+      // of block g - kStages are done
+      if (C::kXPre && !wrole) pf_wait<COMET_PF_SLEEP & 1>(&mdone[g % C::kStages], ((g / C::kStages) & 1) ^ 1);
       if (elect_one()) trace(tr_cta, wrole ? 14 : 15, g);
       if (!kAccOut && !wrole) pf_wait<COMET_PF_SLEEP & 1>(&sempty[a], ((g / C::kScaleSlots) & 1) ^ 1);
       const uint32_t code = map.code[b];
@@ -316,9 +338,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
           // 128-row slab
           const int R = pn0 + C::kRows * (int)crank;
           const int v = max(0, min(C::kRows, args.N - R));
-          mbar_arrive_expect_tx(&lfull[l], COMET_PF_EXP == 5 ? 0 : v * 64);
+          mbar_arrive_expect_tx(&lfull[l], (COMET_PF_EXP == 5 || (COMET_PF_NOLOAD & 2)) ? 0 : v * 64);
           uint8_t* dst = smem + C::kWPBase + l * C::kWPBytes;
-          int r = R, left = COMET_PF_EXP == 5 ? 0 : v;
+          int r = R, left = (COMET_PF_EXP == 5 || (COMET_PF_NOLOAD & 2)) ? 0 : v;
           while (left > 0) {
             const int in_slab = min(left, 128 - (r & 127));
             bulk_load(dst, args.Wq + ((int64_t)(r >> 7) * nb + b) * 8192 + (r & 127) * 64, in_slab * 64, &lfull[l]);
@@ -333,14 +355,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
           // COMET_PF_SXCHAIN: the scales complete on the load-ring barrier with
           // the tokens; the promotion reads them after the block's tfull, which
           // follows lfull through staging -> ready -> MMA -> commit
-          mbar_arrive_expect_tx(&lfull[l], (COMET_PF_EXP >= 5 ? 0 : (is8 ? 128 * 128 : 128 * 64)) +
+          mbar_arrive_expect_tx(&lfull[l], (COMET_PF_EXP >= 5 || (COMET_PF_NOLOAD & 1) ? 0 : (is8 || C::kXPre ? 128 * 128 : 128 * 64)) +
                                                (COMET_PF_SXCHAIN ? ((COMET_PF_NOSX ? 0 : nsx) + nsw) * 4 : 0));
-          uint8_t* xs = smem + C::kXBase + l * C::kXStageBytes;
-          if (COMET_PF_EXP >= 5) {  // 5: no operand loads, 6: no token loads
+          uint8_t* xs = C::kXPre ? smem + C::kABase + (g % C::kStages) * C::kAStageBytes
+                                 : smem + C::kXBase + l * C::kXStageBytes;
+          if (COMET_PF_EXP >= 5 || (COMET_PF_NOLOAD & 1)) {  // 5: no operand loads, 6: no token loads
           } else if (is8)
             tma_load_2d(xs, &tmX8, &lfull[l], rank * 128, my_m0);
           else
-            tma_load_2d(xs, &tmX4, &lfull[l], rank * 64, my_m0);
+            tma_load_2d(xs, &tmX4, &lfull[l], rank * (C::kXPre ? 128 : 64), my_m0);
           if (!kAccOut) {
             uint64_t* sb = COMET_PF_SXCHAIN ? &lfull[l] : &sfull[a];
             if (!COMET_PF_SXCHAIN) mbar_arrive_expect_tx(&sfull[a], (nsx + nsw) * 4);
@@ -380,9 +403,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
         const uint32_t bst = sbase + s * C::kWEBytes;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          mma_i8_ts_2sm(tmem_base + acc * C::kAccCols, a_tm + 8 * k,
-                        umma_desc_sw128_kmajor(bst + h * (C::kRows / C::kItems) * 128 + 32 * k), idesc,
-                        (kPfMagic || k > 0) ? 1u : 0u);
+          if (C::kXPre)
+            mma_i8_ss_2sm(tmem_base + acc * C::kAccCols,
+                          umma_desc_sw128_kmajor(sbase + C::kABase + s * C::kAStageBytes + 32 * k),
+                          umma_desc_sw128_kmajor(bst + h * (C::kRows / C::kItems) * 128 + 32 * k), idesc,
+                          (kPfMagic || k > 0) ? 1u : 0u);
+          else
+            mma_i8_ts_2sm(tmem_base + acc * C::kAccCols, a_tm + 8 * k,
+                          umma_desc_sw128_kmajor(bst + h * (C::kRows / C::kItems) * 128 + 32 * k), idesc,
+                          (kPfMagic || k > 0) ? 1u : 0u);
           if (k == 0 && g < 32) trace(tr_cta, 4, 32 + g);
         }
         if (g < 32) trace(tr_cta, 5, 32 + g);
@@ -395,8 +424,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
   }  // warp 19: idle
   } else if (warp >= C::kStageWarp && warp < C::kStageWarp + C::kStageWarps) {
     if (COMET_PF_REGS) setmaxnreg_dec<64>();
-    const bool do_tok = !C::kStage6 || (warp >= C::kTokWarp && warp < C::kTokWarp + 4);
-    const bool do_w = !C::kStage6 || !do_tok;
+    const bool do_tok = !C::kXPre && (!C::kStage6 || (warp >= C::kTokWarp && warp < C::kTokWarp + 4));
+    const bool do_w = !C::kStage6 || (warp < C::kTokWarp || warp >= C::kTokWarp + 4);
     // ---- warps 12-15: a4 staging (thread = token row of lane quarter q) ----
     const int q = warp & 3;
     // weight-expanding thread index 0 .. kWThreads-1
@@ -844,6 +873,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
   cluster_sync();
   tc_fence_after();
   if (warp == C::kMmaWarp) tmem_dealloc_2sm<512>(tmem_base);
+}
+
+// XPRE: INT4 token plane [M x n4*64 B] -> INT8 x16 [M x n4*128 B], each
+// 4-byte word w -> (w & 0x0F0F0F0F) << 4 | (w & 0xF0F0F0F0) << 32 (the byte
+// order the staging warps write into the A operand)
+__global__ void __launch_bounds__(256) expand_int4_tokens_kernel(const uint4* __restrict__ in,
+                                                                 uint4* __restrict__ out, int64_t n16) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 w = __ldg(in + i);
+    uint4 o0, o1;
+    zext_word(w.x, o0.x, o0.y);
+    zext_word(w.y, o0.z, o0.w);
+    zext_word(w.z, o1.x, o1.y);
+    zext_word(w.w, o1.z, o1.w);
+    out[2 * i] = o0;
+    out[2 * i + 1] = o1;
+  }
 }
 
 }  // namespace comet
