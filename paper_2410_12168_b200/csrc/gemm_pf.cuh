@@ -4,31 +4,31 @@
 //
 // Pair tile: 256 tokens (MMA M; 128 TMEM lanes in each CTA) x 192 weight rows
 // (each CTA stages 96 of them in smem).  K is walked one 128-channel FMPQ
-// block at a time.  Each block is issued as two N=96
-// "items" (the two 48-row halves of each CTA's weight rows), each into one of
-// four 96-column INT32 accumulators, so the promotion of item i overlaps the
-// MMAs of items i+1..i+3 (the paper's two-level overlap of conversion and
-// MMA, re-cut for TMEM).
+// block at a time; each block is one MMA item of 4 x
+// tcgen05.mma.cta_group::2.kind::i8 (M=256, N=192, K=32) into one of two
+// 192-column INT32 accumulators, so the promotion of block b overlaps the MMAs
+// of block b+1 (the paper's overlap of conversion and MMA, P:L255-259,
+// re-cut for TMEM).  TMEM: 2 x 192 accumulator + 4 x 32 A-slot columns.
 //
-// Roles per CTA (16 warps = 512 threads: the register file gives every
-// thread 128 registers, 64 of which hold the promotion's fp32 running sums):
-//   warps 12-15 (a4 staging; thread = token row of the warp's TMEM lane
-//       quarter): per block the row's token block -- zero-extended INT4 (x16,
-//       P:L294) or raw INT8 -- goes from smem through registers into the
-//       block's TMEM A slot (tcgen05.st), and 3 chunks of the packed weight
-//       rows are zero-extended into the SW128 K-major B operand in smem;
-//     warp 12 also is the producer (a3): kLoadAhead blocks ahead, 1-D bulk
-//       copies of the CTA's 96 packed weight rows (tiled layout, 64B swizzle
-//       baked in), a TMA of the token slab (INT8 blocks [128 x 128 B] SW128,
-//       INT4 blocks packed [128 x 64 B] SW64), 1-D copies of the scales;
-//     warp 13 of the leader also issues the MMAs (a5), kMmaLag blocks behind
-//       its staging: per item 4 x tcgen05.mma.cta_group::2.kind::i8 (A from
-//       TMEM, M=256, N=96, K=32) into a fresh accumulator, commit multicast;
-//   warps 0-11 (a6, a8; thread = token row): promote 2 x 32 columns of each
-//       block (16-column units 2k, 2k+1 of both items, k = warp / 4):
-//       tcgen05.ld of 32 columns, I2F, fma.rn.f32x2 with the thread-uniform
-//       row scale; per-channel weight scales are applied once per tile; at
-//       the tile's last block fp16 RNE -> smem -> TMA tensor stores.
+// Roles per CTA (20 warps = 640 threads, 96 registers; lower warp ids first):
+//   warps 0 / 2 (a3 producers): weights -- 1-D bulk copies of the CTA's 96
+//       packed rows (tiled layout, 64B swizzle baked in) -- and tokens -- a
+//       TMA of the block's token slab (INT8 [128 x 128 B] SW128, INT4
+//       [128 x 64 B] SW64) plus 1-D copies of the scales; a 5-deep load ring;
+//   warp 1 of the leader (a5): waits the block's `ready` and the accumulator's
+//       `tempty`, issues the 4 MMAs, commits to both CTAs (warp 3 idles);
+//   warps 4-7 (a4 staging; thread = token row of the warp's TMEM lane
+//       quarter): the row's token block -- zero-extended INT4 (x16) or
+//       raw INT8 -- goes from smem through registers into the block's TMEM A
+//       slot (tcgen05.st), and 3 chunks of the packed weight rows are
+//       zero-extended into the SW128 K-major B operand; a 4-deep operand ring;
+//   warps 8-19 (a6, a8; thread = token row, 64 columns): double-buffered
+//       8-column tcgen05.ld, I2F + fma.rn.f32x2 with the thread-uniform row
+//       scale; per-channel weight scales once per tile; at the tile's last
+//       block fp16 RNE -> smem -> TMA tensor stores.
+// Compile-time switches (DESIGN.md section 7 lists what each measured):
+// COMET_PF_XPRE (pre-expanded INT4 tokens, SS MMA), COMET_PF_TILEN /
+// COMET_PF_ACCS / COMET_PF_PQ (tile shape), COMET_PF_EXP (timing skeletons).
 #pragma once
 #include <cuda_fp16.h>
 #include <stdint.h>
@@ -93,25 +93,11 @@ DEVI void pf_wait_cluster(uint64_t* bar, uint32_t parity) {
 #define COMET_PF_EXP 0  // timing experiments only (wrong results): 1 = skip staging work, 2 = skip promotion math, 3 = both, 4 = also skip the accumulator loads, 5 = also skip the operand loads
 #endif
 
-#ifndef COMET_PF_NOSX
-#define COMET_PF_NOSX 0  // timing experiment: skip the activation-scale loads (wrong results)
-#endif
-#ifndef COMET_PF_NOLOAD
-#define COMET_PF_NOLOAD 0  // timing experiment (wrong results): 1 = no token TMA, 2 = no weight copies
-#endif
-#ifndef COMET_PF_REGS
-#define COMET_PF_REGS 0  // 1: setmaxnreg rebalancing (promotion 120 / staging 64 / producers+MMA 40); ptxas
-                         // still pipelines the accumulator loads 3 deep, so no gain -- and the pool is the
-                         // launch allocation (96 x 640), not 64K: a larger inc deadlocks
-#endif
 #ifndef COMET_PF_SXCHAIN
 #define COMET_PF_SXCHAIN 1  // scales complete on the load-ring barrier (no scale barrier wait in the promotion)
 #endif
 #ifndef COMET_PF_XPRE
 #define COMET_PF_XPRE 0
-#endif
-#ifndef COMET_PF_STPIPE
-#define COMET_PF_STPIPE 0  // 1: staging warps prefetch the next block's shared-memory operands (measured 9% slower)
 #endif
 #ifndef COMET_PF_LDPIPE
 #define COMET_PF_LDPIPE 1  // double-buffered 8-column accumulator loads in the promotion
@@ -181,29 +167,17 @@ struct PfCfg {
   // warp order = scheduling priority among the warps of an SMSP (lower ids
   // win when several are ready): the latency-critical role warps (producers,
   // MMA issuer) and the staging warps first, the promotion warps last
-#ifndef COMET_PF_STAGE6
-#define COMET_PF_STAGE6 0  // measured -6% (21 warps round to 24: 80 registers)
-#endif
-  // STAGE6 (roles first only): 6 staging warps -- warps 4..7 expand tokens
-  // into TMEM (one per lane quarter), warps 3 and 8 expand weights into smem --
-  // instead of 4 doing both; 3 role warps (no idle warp), promotion warps 9..20:
-  // 21 warps still leave 96 registers per thread
-  static constexpr bool kStage6 = COMET_PF_STAGE6 && COMET_PF_ROLES_FIRST;
-  static constexpr int kStageWarps = kStage6 ? 6 : 4;
-  static constexpr int kRoleWarps = kStage6 ? 3 : 4;
-  static constexpr int kRoleBase = COMET_PF_ROLES_FIRST ? 0 : kPWarps + kStageWarps;  // role warps
-  static constexpr int kStageWarp = COMET_PF_ROLES_FIRST ? kRoleWarps : kPWarps;    // staging warps
-  static constexpr int kTokWarp = kStage6 ? 4 : kStageWarp;                          // first token warp
-  static constexpr int kPBase = COMET_PF_ROLES_FIRST ? kRoleWarps + kStageWarps : 0;  // promotion warps
-  static constexpr int kWThreads = kStage6 ? 64 : 128;                               // weight-expanding threads
+  static constexpr int kRoleBase = COMET_PF_ROLES_FIRST ? 0 : kPWarps + 4;  // 4 role warps
+  static constexpr int kStageWarp = COMET_PF_ROLES_FIRST ? 4 : kPWarps;     // 4 staging warps
+  static constexpr int kPBase = COMET_PF_ROLES_FIRST ? 8 : 0;               // promotion warps
   static constexpr int kLoadWarp = kRoleBase;        // weights
   static constexpr int kMmaWarp = kRoleBase + 1;
 #ifndef COMET_PF_XWARP
 #define COMET_PF_XWARP 6  // 7: token producer on the 4th SMSP (measured neutral)
 #endif
   static constexpr int kLoad2Warp = kRoleBase + COMET_PF_XWARP - 4;  // tokens + scales (the 4th warp idles)
-  static constexpr int kThreads = 32 * (kPWarps + kRoleWarps + kStageWarps);
-  static constexpr int kReadyCount = 2 * kStageWarps;  // both CTAs' staging warps
+  static constexpr int kThreads = 32 * (kPWarps + 8);
+  static constexpr int kReadyCount = 2 * 4;  // both CTAs' staging warps
   static constexpr int kTemptyCount = 2 * kPWarps;   // both CTAs' promotion warps
 };
 
@@ -263,7 +237,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
     }
     for (int l = 0; l < C::kLStages; ++l) {
       mbar_init(&lfull[l], 2);  // two producers
-      mbar_init(&lempty[l], C::kStageWarps);
+      mbar_init(&lempty[l], 4);
     }
     for (int a = 0; a < C::kAccs; ++a) {
       mbar_init(&tfull[a], 1);
@@ -292,12 +266,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
   const bool tr_cta = kTraceBuild && g_cta_times_on && blockIdx.x + 1 == g_cta_times_on;
   const bool tr_pair = kTraceBuild && g_cta_times_on && (blockIdx.x >> 1) == ((g_cta_times_on - 1) >> 1);
 
-  // register rebalancing per warpgroup (the launch pool 96 x 640 = 3 x 128 x 120
-  // + 128 x 64 + 128 x 40 + slack; every warp of a warpgroup executes the same setmaxnreg, inside
-  // the warpgroup's branch so ptxas allocates each role's code to its budget):
-  // the promotion warps hold the running sums (64) and 7 accumulator chunks
-  if (warp >= C::kRoleBase && warp < C::kRoleBase + C::kRoleWarps) {
-  if (COMET_PF_REGS) setmaxnreg_dec<40>();
+  // (setmaxnreg rebalancing does not help here: ptxas compiles every role to
+  // the launch budget of 96 registers, and 24+ warps drop it to 80)
+  if (warp >= C::kRoleBase && warp < C::kRoleBase + 4) {
   if (warp == C::kLoadWarp || warp == C::kLoad2Warp) {
     // ------------------- a3: producers (weights | tokens + scales) ----
     // two warps: each TMA / bulk-copy issue costs the issuing thread ~10^2
@@ -338,9 +309,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
           // 128-row slab
           const int R = pn0 + C::kRows * (int)crank;
           const int v = max(0, min(C::kRows, args.N - R));
-          mbar_arrive_expect_tx(&lfull[l], (COMET_PF_EXP == 5 || (COMET_PF_NOLOAD & 2)) ? 0 : v * 64);
+          mbar_arrive_expect_tx(&lfull[l], COMET_PF_EXP == 5 ? 0 : v * 64);
           uint8_t* dst = smem + C::kWPBase + l * C::kWPBytes;
-          int r = R, left = (COMET_PF_EXP == 5 || (COMET_PF_NOLOAD & 2)) ? 0 : v;
+          int r = R, left = COMET_PF_EXP == 5 ? 0 : v;
           while (left > 0) {
             const int in_slab = min(left, 128 - (r & 127));
             bulk_load(dst, args.Wq + ((int64_t)(r >> 7) * nb + b) * 8192 + (r & 127) * 64, in_slab * 64, &lfull[l]);
@@ -355,11 +326,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
           // COMET_PF_SXCHAIN: the scales complete on the load-ring barrier with
           // the tokens; the promotion reads them after the block's tfull, which
           // follows lfull through staging -> ready -> MMA -> commit
-          mbar_arrive_expect_tx(&lfull[l], (COMET_PF_EXP >= 5 || (COMET_PF_NOLOAD & 1) ? 0 : (is8 || C::kXPre ? 128 * 128 : 128 * 64)) +
-                                               (COMET_PF_SXCHAIN ? ((COMET_PF_NOSX ? 0 : nsx) + nsw) * 4 : 0));
+          mbar_arrive_expect_tx(&lfull[l], (COMET_PF_EXP >= 5 ? 0 : (is8 || C::kXPre ? 128 * 128 : 128 * 64)) +
+                                               (COMET_PF_SXCHAIN ? (nsx + nsw) * 4 : 0));
           uint8_t* xs = C::kXPre ? smem + C::kABase + (g % C::kStages) * C::kAStageBytes
                                  : smem + C::kXBase + l * C::kXStageBytes;
-          if (COMET_PF_EXP >= 5 || (COMET_PF_NOLOAD & 1)) {  // 5: no operand loads, 6: no token loads
+          if (COMET_PF_EXP >= 5) {  // 5: no operand loads, 6: no token loads
           } else if (is8)
             tma_load_2d(xs, &tmX8, &lfull[l], rank * 128, my_m0);
           else
@@ -368,7 +339,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
             uint64_t* sb = COMET_PF_SXCHAIN ? &lfull[l] : &sfull[a];
             if (!COMET_PF_SXCHAIN) mbar_arrive_expect_tx(&sfull[a], (nsx + nsw) * 4);
             uint8_t* slot = smem + C::kScaleBase + a * C::kSlotBytes;
-            if (nsx && !COMET_PF_NOSX) bulk_load(slot, args.Sx + (int64_t)b * args.ldsx + my_m0, nsx * 4, sb);
+            if (nsx) bulk_load(slot, args.Sx + (int64_t)b * args.ldsx + my_m0, nsx * 4, sb);
             if (nsw) bulk_load(slot + C::kSwOff, args.Sw + (kGroupK ? 0 : (int64_t)b * args.N) + pn0, nsw * 4, sb);
           }
         }
@@ -422,108 +393,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
       __syncwarp();
     }
   }  // warp 19: idle
-  } else if (warp >= C::kStageWarp && warp < C::kStageWarp + C::kStageWarps) {
-    if (COMET_PF_REGS) setmaxnreg_dec<64>();
-    const bool do_tok = !C::kXPre && (!C::kStage6 || (warp >= C::kTokWarp && warp < C::kTokWarp + 4));
-    const bool do_w = !C::kStage6 || (warp < C::kTokWarp || warp >= C::kTokWarp + 4);
-    // ---- warps 12-15: a4 staging (thread = token row of lane quarter q) ----
+  } else if (warp >= C::kStageWarp && warp < C::kStageWarp + 4) {
+    // ---- a4 staging (thread = token row of lane quarter q) ----
+    // (XPRE: the tokens arrive expanded in smem; only the weights are staged)
+    constexpr bool do_tok = !C::kXPre, do_w = true;
     const int q = warp & 3;
-    // weight-expanding thread index 0 .. kWThreads-1
-    const int et = C::kStage6 ? lane + (warp == C::kStageWarp ? 0 : 32) : (int)threadIdx.x - 32 * C::kStageWarp;
+    const int et = (int)threadIdx.x - 32 * C::kStageWarp;  // weight-expanding thread 0..127
     const uint32_t tst = tmem_base + ((uint32_t)(32 * q) << 16) + C::kAOff;
     const uint32_t leader_ready = mapa_shared(smem_u32(ready), 0);
-    if (COMET_PF_STPIPE && COMET_PF_EXP == 0) {
-      // software-pipelined: the shared-memory loads of block j + 1 are issued
-      // right after block j's operands are written, so their latency overlaps
-      // block j's hand-off (fence, TMEM-store wait, ready arrive) and the next
-      // block's barrier waits instead of following them
-      constexpr int kWC4 = C::kRows * 4 / C::kWThreads;
-      const uint32_t r_ = (32 * q) + (opaque(threadIdx.x) & 31);  // this thread's token row
-      auto load_block = [&](int jj, bool is8j, uint4(&tv)[8], uint4(&wv)[kWC4]) {
-        const int l = jj % C::kLStages;
-        const uint32_t xs = sbase + C::kXBase + l * C::kXStageBytes;
-        const uint32_t wps = sbase + C::kWPBase + l * C::kWPBytes;
-        pf_wait<COMET_PF_SLEEP & 4>(&lfull[l], (jj / C::kLStages) & 1);
-        if (!do_tok) {
-        } else if (is8j) {
-#pragma unroll
-          for (int c = 0; c < 8; ++c) tv[c] = lds128(xs + r_ * 128 + ((c ^ (r_ & 7)) << 4));
-        } else {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) tv[c] = lds128(xs + r_ * 64 + ((c ^ ((r_ >> 1) & 3)) << 4));
-        }
-#pragma unroll
-        for (int k = 0; k < kWC4 && do_w; ++k) {
-          const int ch = et + C::kWThreads * k;
-          const int er = ch >> 2, ej = ch & 3;
-          wv[k] = lds128(wps + er * 64 + ((ej ^ ((er >> 1) & 3)) << 4));
-        }
-      };
-      auto stage_block = [&](int jj, bool is8j, uint4(&tv)[8], uint4(&wv)[kWC4], bool is8n,
-                             uint4(&tvn)[8], uint4(&wvn)[kWC4]) {
-        const int l = jj % C::kLStages, s = jj % C::kStages;
-        const uint32_t wst = sbase + s * C::kWEBytes;
-        // operand stage s (smem B + TMEM A slot) is free once the MMAs of
-        // block jj - kStages are done
-        pf_wait<COMET_PF_SLEEP & 4>(&mdone[s], ((jj / C::kStages) & 1) ^ 1);
-        trace(tr_cta && threadIdx.x == 32 * C::kTokWarp, 10, jj);
-        tc_fence_after();
-        if (do_tok) {  // tokens: 4 chunks of 32 K = 32 TMEM A columns (INT8 raw, INT4 x16)
-          uint32_t e[32];
-          if (is8j) {
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              e[4 * c] = tv[c].x; e[4 * c + 1] = tv[c].y; e[4 * c + 2] = tv[c].z; e[4 * c + 3] = tv[c].w;
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              zext_word(tv[c].x, e[8 * c + 0], e[8 * c + 1]);
-              zext_word(tv[c].y, e[8 * c + 2], e[8 * c + 3]);
-              zext_word(tv[c].z, e[8 * c + 4], e[8 * c + 5]);
-              zext_word(tv[c].w, e[8 * c + 6], e[8 * c + 7]);
-            }
-          }
-          tmem_st_32x32b_x32(tst + 32 * s, e);
-        }
-#pragma unroll
-        for (int k = 0; k < kWC4 && do_w; ++k) {  // weights -> SW128 B operand
-          const int ch = et + C::kWThreads * k;
-          const int er = ch >> 2, ej = ch & 3;
-          expand_chunk(wv[k], wst + er * 128 + (((2 * ej) ^ (er & 7)) << 4),
-                       wst + er * 128 + (((2 * ej + 1) ^ (er & 7)) << 4));
-        }
-        // the load stage may be refilled once every lane's loads have been
-        // consumed (by the tcgen05.st / st.shared above)
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&lempty[l]);
-        fence_proxy_async_smem();
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(leader_ready + s * 8);
-        trace(tr_cta && threadIdx.x == 32 * C::kTokWarp, 1, jj);
-        // (after the fence: a proxy fence waits for the warp's outstanding
-        // shared-memory loads)
-        if (jj + 1 < steps) load_block(jj + 1, is8n, tvn, wvn);
-      };
-      int sb = 0;
-      auto next_is8 = [&]() {
-        const bool r = (map.code[sb] >> 15) != 0;
-        if (++sb == nb) sb = 0;
-        return r;
-      };
-      // one register set: block j's operands are consumed before block j + 1's
-      // loads are issued into the same registers
-      uint4 tv[8], wv[kWC4];
-      bool is8 = next_is8();
-      if (steps > 0) load_block(0, is8, tv, wv);
-      for (int j = 0; j < steps; ++j) {
-        const bool is8n = next_is8();  // block j + 1
-        stage_block(j, is8, tv, wv, is8n, tv, wv);
-        is8 = is8n;
-      }
-    } else {
     int sb = 0;
     for (int j = 0; j < steps; ++j) {
       // ---- a4: stage block j: load stage l -> operand stage s ----
@@ -534,11 +411,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
       const uint32_t wps = sbase + C::kWPBase + l * C::kWPBytes;
       const uint32_t wst = sbase + s * C::kWEBytes;
       pf_wait<COMET_PF_SLEEP & 4>(&lfull[l], (j / C::kLStages) & 1);
-      trace(tr_cta && threadIdx.x == 32 * C::kTokWarp, 12, j);
+      trace(tr_cta && threadIdx.x == 32 * C::kStageWarp, 12, j);
       // operand stage s (smem B + TMEM A slot) is free once the MMAs of block
       // j - kStages are done
       pf_wait<COMET_PF_SLEEP & 4>(&mdone[s], ((j / C::kStages) & 1) ^ 1);
-      trace(tr_cta && threadIdx.x == 32 * C::kTokWarp, 10, j);
+      trace(tr_cta && threadIdx.x == 32 * C::kStageWarp, 10, j);
       tc_fence_after();
       if (COMET_PF_EXP != 1 && COMET_PF_EXP < 3) {
       // all shared-memory loads of the block first (the loads and stores are
@@ -554,17 +431,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) tv[c] = lds128(xs + r_ * 64 + ((c ^ ((r_ >> 1) & 3)) << 4));
       }
-      uint4 wv[C::kRows * 4 / C::kWThreads];
+      uint4 wv[C::kRows * 4 / 128];
 #pragma unroll
-      for (int k = 0; k < C::kRows * 4 / C::kWThreads && do_w; ++k) {
-        const int ch = et + C::kWThreads * k;
+      for (int k = 0; k < C::kRows * 4 / 128 && do_w; ++k) {
+        const int ch = et + 128 * k;
         const int er = ch >> 2, ej = ch & 3;
         wv[k] = lds128(wps + er * 64 + ((ej ^ ((er >> 1) & 3)) << 4));
       }
       if (kTraceBuild) {  // the LDS results have landed
         uint32_t dep = tv[0].x ^ tv[3].w;
-        if (do_w) dep ^= wv[0].x ^ wv[C::kRows * 4 / C::kWThreads - 1].w;
-        trace(tr_cta && threadIdx.x == 32 * C::kTokWarp && dep != 0x9e3779b9u, 16, j);
+        if (do_w) dep ^= wv[0].x ^ wv[C::kRows * 4 / 128 - 1].w;
+        trace(tr_cta && threadIdx.x == 32 * C::kStageWarp && dep != 0x9e3779b9u, 16, j);
       }
       // tokens: 4 chunks of 32 K = 32 TMEM A columns (INT8 raw, INT4 x16)
       if (do_tok) {
@@ -587,15 +464,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
           uint32_t dep = 0;
 #pragma unroll
           for (int x = 0; x < 32; ++x) dep ^= e[x];
-          trace(tr_cta && threadIdx.x == 32 * C::kTokWarp && dep != 0x9e3779b9u, 13, j);
+          trace(tr_cta && threadIdx.x == 32 * C::kStageWarp && dep != 0x9e3779b9u, 13, j);
         }
         tmem_st_32x32b_x32(tst + 32 * s, e);
       }
-      trace(kTraceEv2 && tr_cta && threadIdx.x == 32 * C::kTokWarp, 6, j);
+      trace(kTraceEv2 && tr_cta && threadIdx.x == 32 * C::kStageWarp, 6, j);
       // weights: chunks et, et + 128, et + 256 of the packed slab -> SW128 B operand
 #pragma unroll
-      for (int k = 0; k < C::kRows * 4 / C::kWThreads && do_w; ++k) {
-        const int ch = et + C::kWThreads * k;
+      for (int k = 0; k < C::kRows * 4 / 128 && do_w; ++k) {
+        const int ch = et + 128 * k;
         const int er = ch >> 2, ej = ch & 3;
         expand_chunk(wv[k], wst + er * 128 + (((2 * ej) ^ (er & 7)) << 4), wst + er * 128 + (((2 * ej + 1) ^ (er & 7)) << 4));
       }
@@ -605,19 +482,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
       // the LDS instructions could overtake them)
       __syncwarp();
       if (lane == 0) mbar_arrive(&lempty[l]);
-      trace(kTraceEv2 && tr_cta && threadIdx.x == 32 * C::kTokWarp, 9, j);
+      trace(kTraceEv2 && tr_cta && threadIdx.x == 32 * C::kStageWarp, 9, j);
       fence_proxy_async_smem();
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_ready + s * 8);
-      trace(tr_cta && threadIdx.x == 32 * C::kTokWarp, 1, j);
-    }
+      trace(tr_cta && threadIdx.x == 32 * C::kStageWarp, 1, j);
     }
   } else {
-    if (COMET_PF_REGS) setmaxnreg_inc<120>();
 
-    // ------------------------ warps 0-11: a6 promotion + a8 write-back ----
+    // ----------------------- warps 8-19: a6 promotion + a8 write-back ----
     const int q = warp & 3;         // TMEM lane quarter
     const int kw = (warp - C::kPBase) >> 2;  // 0..kPQ-1: item columns [kWCols kw, kWCols (kw + 1)) of every item
     const int row = 32 * q + lane;  // token row within this CTA
@@ -711,26 +586,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
             }
           };
           constexpr int kC = kWC / 8;
-          if (COMET_PF_REGS) {
-            // setmaxnreg gave this warpgroup 120 registers: 7 of the 8 chunks
-            // are loaded at once, the 8th into the first chunk's registers
-            // after its promotion, and the accumulator is released right
-            // after -- its hold time is the load stream plus one chunk of math
-            uint32_t rq[7][8];
-#pragma unroll
-            for (int c = 0; c < 7; ++c) tmem_ld_32x32b_x8(ta + 8 * c, rq[c]);
-#pragma unroll
-            for (int c = 0; c < 7; ++c) tmem_ld_wait_dep(rq[c]);
-            promote8(0, rq[0]);
-            tmem_ld_32x32b_x8(ta + 56, rq[0]);
-            tmem_ld_wait_dep(rq[0]);
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(leader_tempty + acc * 8);
-#pragma unroll
-            for (int c = 1; c < 7; ++c) promote8(c, rq[c]);
-            promote8(7, rq[0]);
-          } else {
           uint32_t ra[8], rb[8];
           tmem_ld_32x32b_x8(ta, ra);
           tmem_ld_wait_dep(ra);
@@ -750,7 +605,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
             }
             promote8(c + 1, rb);
             if (c + 2 < kC) tmem_ld_wait_dep(ra);
-          }
           }
         } else {
           // 16 columns per tcgen05.ld (the running sums leave room for 16);
