@@ -26,6 +26,9 @@ and the SPEC readings listed in DESIGN.md:
   products in IEEE fp32 (the precision the kernels decide the integers in),
   rha = round half away from zero evaluated exactly.
 
+* f4 static per-block activation scales: see
+  static_block_scales / quantize_act_static below.
+
 Parity status: pinned by tests/test_fmpq_aux.py (SPEC worked examples,
 lattice round trips, round-trip bound, brute-force reference of the rules).
 """
@@ -151,3 +154,67 @@ def dequantize_kv(q: np.ndarray, scale: np.ndarray, zp: np.ndarray, group: int) 
     g = np.arange(T) // group
     y = ((q.astype(np.float32) - zp[g].astype(np.float32)).astype(np.float32) * scale[g]).astype(np.float32)
     return y.astype(np.float16)
+
+
+# ------------------------------------------------------------------ f4 ----
+# Static per-block activation scales (SPEC S:L157-165
+# assign_block_precision: "per-block QuantParams computed from the permuted
+# channels' pooled min/max at the block's bit width, symmetric scheme";
+# compute_scale S:L62-70: symmetric scale = max(|min|, |max|) / qmax with
+# qmax = 2^(b-1) - 1, degenerate -> scale 1; quantize S:L71-78:
+# q = clamp(round_half_away(x / scale), -qmax, qmax)).  The runtime absmax of
+# the dynamic path is replaced by one calibrated scale per block, the same for
+# every token row; Sx[b, m] = scale_b so the GEMM is unchanged.
+def static_block_scales(maxabs: np.ndarray, bits, perm=None, k: int = BLOCK) -> np.ndarray:
+    """scale_b = fp32(pool_b / qmax_b), pool_b = max of the calibration maxabs
+    over the block's channels on the permuted axis; pool_b == 0 -> 1."""
+    maxabs = np.asarray(maxabs, dtype=np.float32)
+    K = maxabs.size
+    order = np.arange(K) if perm is None else np.asarray(perm, dtype=np.int64)
+    out = np.zeros(K // k, np.float32)
+    for b in range(K // k):
+        pool = np.float32(max(float(maxabs[order[b * k + i]]) for i in range(k)))
+        qmax = np.float32(127 if int(bits[b]) == 8 else 7)
+        out[b] = np.float32(1.0) if pool == 0 else np.float32(pool / qmax)
+    return out
+
+
+def _q_static(x: np.float32, s: np.float32, qmax: int) -> int:
+    v = np.float32(x / s)  # IEEE fp32 quotient
+    if not np.isfinite(v):
+        return qmax if v > 0 else -qmax
+    return min(qmax, max(-qmax, _rha(v)))
+
+
+def quantize_act_static(X: np.ndarray, bits, scales: np.ndarray, perm=None, k: int = BLOCK):
+    """X fp16 [M x K] -> (Xq8 int8 [M x K8], Xq4 uint8 [M x K4/2], Sx fp32 [nb x ldsx])
+    in the comet plane layout (INT4 nibble order of oracle.pack_int4)."""
+    from . import ldsx_for, pack_int4, plane_widths
+
+    X = np.asarray(X, dtype=np.float16)
+    M, K = X.shape
+    nb = K // k
+    order = np.arange(K) if perm is None else np.asarray(perm, dtype=np.int64)
+    Xp = X.astype(np.float32)[:, order]
+    K8, K4 = plane_widths(bits, k)
+    ldsx = ldsx_for(M)
+    Xq8 = np.zeros((M, K8), np.int8)
+    Xq4 = np.zeros((M, K4 // 2), np.uint8)
+    Sx = np.ones((nb, ldsx), np.float32)
+    r8 = r4 = 0
+    for b in range(nb):
+        is8 = int(bits[b]) == 8
+        qmax = 127 if is8 else 7
+        s = np.float32(scales[b])
+        for m in range(M):
+            q = np.array([_q_static(Xp[m, b * k + i], s, qmax) for i in range(k)], dtype=np.int8)
+            if is8:
+                Xq8[m, r8 * k:(r8 + 1) * k] = q
+            else:
+                Xq4[m, r4 * k // 2:(r4 + 1) * k // 2] = pack_int4(q)
+            Sx[b, m] = s
+        if is8:
+            r8 += 1
+        else:
+            r4 += 1
+    return Xq8, Xq4, Sx
