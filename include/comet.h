@@ -175,6 +175,26 @@ comet_status comet_quantize_kv(const void* KV, int64_t ld, int32_t T, int32_t C,
 comet_status comet_dequantize_kv(const void* Q, const float* scale, const uint8_t* zp, int32_t T, int32_t C,
                                  int32_t group, void* out, int64_t ldo, comet_stream_t stream);
 
+/* ---- f4: static per-block activation scales (SPEC
+ * S:L157-165 "per-block QuantParams computed from the permuted channels'
+ * pooled min/max at the block's bit width, symmetric scheme") ----
+ * comet_static_act_scales: scales (DEVICE fp32[K/128]) with
+ *   scales[b] = fp32(pool_b / qmax_b), qmax_b = 127 (INT8 block) or 7,
+ *   pool_b = max over the block's channels i (permuted axis) of
+ *   maxabs[perm[128 b + i]] (maxabs: DEVICE fp32[K] from comet_calib_absmax;
+ *   perm as in comet_quantize_act, NULL = identity), 1 if pool_b == 0.
+ * comet_quantize_act_static: as comet_quantize_act (same arguments, planes,
+ *   Sx layout) but with the calibrated scales instead of the runtime absmax:
+ *   q = clamp(rha(fp32(x / scales[b])), -qmax_b, qmax_b) (IEEE division,
+ *   round half away from zero; inputs beyond the calibrated range clamp),
+ *   Sx[b*ldsx + m] = scales[b] -- the output feeds comet_w4ax_gemm as is.
+ *   scales: DEVICE fp32[K/128], every entry > 0. */
+comet_status comet_static_act_scales(const float* maxabs, int32_t K, const int32_t* perm, const uint8_t* block_bits,
+                                     float* scales, comet_stream_t stream);
+comet_status comet_quantize_act_static(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
+                                       const uint8_t* block_bits, const float* scales, int8_t* Xq8, void* Xq4,
+                                       float* Sx, int64_t ldsx, comet_stream_t stream);
+
 const char* comet_status_str(comet_status s);
 const char* comet_last_cuda_error(void);
 /* number of kernel launches this library issued since load (host counter) */

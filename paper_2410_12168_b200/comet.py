@@ -24,7 +24,8 @@ STATUS = {0: "COMET_OK", 1: "COMET_ERR_INVALID_ARG", 2: "COMET_ERR_SHAPE", 3: "C
 EXPORTS = ["comet_act_plane8_bytes", "comet_act_plane4_bytes", "comet_act_ldsx", "comet_w4ax_gemm_workspace_bytes",
            "comet_w4ax_linear_scratch_bytes", "comet_pack_weight", "comet_quantize_act", "comet_w4ax_gemm",
            "comet_w4ax_gemm_acc_i32", "comet_w4ax_linear", "comet_calib_absmax", "comet_fmpq_map",
-           "comet_quantize_kv", "comet_dequantize_kv", "comet_status_str", "comet_last_cuda_error",
+           "comet_quantize_kv", "comet_dequantize_kv", "comet_static_act_scales", "comet_quantize_act_static",
+           "comet_status_str", "comet_last_cuda_error",
            "comet_launch_count"]
 
 
@@ -77,6 +78,10 @@ def lib():
         L.comet_quantize_kv.restype = ctypes.c_int
         L.comet_dequantize_kv.argtypes = [P, P, P, i32, i32, i32, P, i64, P]
         L.comet_dequantize_kv.restype = ctypes.c_int
+        L.comet_static_act_scales.argtypes = [P, i32, P, P, P, P]
+        L.comet_static_act_scales.restype = ctypes.c_int
+        L.comet_quantize_act_static.argtypes = [P, i64, i32, i32, P, P, P, P, P, P, i64, P]
+        L.comet_quantize_act_static.restype = ctypes.c_int
         L.comet_status_str.argtypes = [ctypes.c_int]
         L.comet_status_str.restype = ctypes.c_char_p
         L.comet_last_cuda_error.argtypes = []
@@ -188,6 +193,33 @@ def comet_quantize_act(X: torch.Tensor, bits, perm: Optional[torch.Tensor] = Non
     st = lib().comet_quantize_act(_ptr(X), X.stride(0), M, K, _ptr(perm), b.ptr, _ptr(Xq8) if b.n8 else None,
                                   _ptr(Xq4) if b.n4 else None, _ptr(Sx), Sx.shape[1], _stream(stream))
     _check("comet_quantize_act", st)
+    return Xq8, Xq4, Sx
+
+
+def comet_static_act_scales(maxabs: torch.Tensor, bits, perm: Optional[torch.Tensor] = None, stream=None):
+    """f4: static per-block activation scales (DEVICE fp32[K/128]) from the
+    calibration maxabs (DEVICE fp32[K]) -- see comet.h."""
+    assert maxabs.is_cuda and maxabs.dtype == torch.float32 and maxabs.dim() == 1
+    b = as_bits(bits)
+    K = maxabs.shape[0]
+    scales = torch.empty(K // BLOCK, dtype=torch.float32, device=maxabs.device)
+    st = lib().comet_static_act_scales(_ptr(maxabs), K, _ptr(perm), b.ptr, _ptr(scales), _stream(stream))
+    _check("comet_static_act_scales", st)
+    return scales
+
+
+def comet_quantize_act_static(X: torch.Tensor, bits, scales: torch.Tensor, perm: Optional[torch.Tensor] = None,
+                              out=None, stream=None):
+    """f4: X fp16 [M x K] -> (Xq8, Xq4, Sx) with the static per-block scales."""
+    assert X.is_cuda and X.dtype == torch.float16 and X.dim() == 2 and X.stride(1) == 1
+    assert scales.is_cuda and scales.dtype == torch.float32
+    b = as_bits(bits)
+    M, K = X.shape
+    Xq8, Xq4, Sx = out if out is not None else alloc_act_planes(M, K, b, X.device)
+    st = lib().comet_quantize_act_static(_ptr(X), X.stride(0), M, K, _ptr(perm), b.ptr, _ptr(scales),
+                                         _ptr(Xq8) if b.n8 else None, _ptr(Xq4) if b.n4 else None, _ptr(Sx),
+                                         Sx.shape[1], _stream(stream))
+    _check("comet_quantize_act_static", st)
     return Xq8, Xq4, Sx
 
 

@@ -646,6 +646,75 @@ comet_status comet_calib_absmax(const void* X, int64_t ldx, int32_t M, int32_t K
   return check_launch();
 }
 
+comet_status comet_static_act_scales(const float* maxabs, int32_t K, const int32_t* perm, const uint8_t* block_bits,
+                                     float* scales, comet_stream_t stream) {
+  if (!block_bits || K <= 0) return COMET_ERR_INVALID_ARG;
+  if (K % 128 || K > 65536) return COMET_ERR_SHAPE;
+  BlockMap map;
+  int n8 = 0, n4 = 0;
+  if (!build_block_map(block_bits, K / 128, &map, &n8, &n4)) return COMET_ERR_INVALID_ARG;
+  if (!maxabs || !scales) return COMET_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(maxabs) & 3) || (reinterpret_cast<uintptr_t>(scales) & 3) ||
+      (reinterpret_cast<uintptr_t>(perm) & 3))
+    return COMET_ERR_ALIGNMENT;
+  comet_status ds = device_check(nullptr);
+  if (ds != COMET_OK) return ds;
+  static_act_scales_kernel<<<K / 128, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(maxabs, perm, map, scales);
+  return check_launch();
+}
+
+comet_status comet_quantize_act_static(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
+                                       const uint8_t* block_bits, const float* scales, int8_t* Xq8, void* Xq4,
+                                       float* Sx, int64_t ldsx, comet_stream_t stream) {
+  if (M < 0 || K <= 0 || !block_bits) return COMET_ERR_INVALID_ARG;
+  if (K % 128 || K > 65536 || ldx < K || ldx % 8 || ldsx < M || ldsx % 4) return COMET_ERR_SHAPE;
+  BlockMap map;
+  int n8 = 0, n4 = 0;
+  if (!build_block_map(block_bits, K / 128, &map, &n8, &n4)) return COMET_ERR_INVALID_ARG;
+  if (M == 0) return COMET_OK;
+  if (!X || !Sx || !scales || (n8 && !Xq8) || (n4 && !Xq4)) return COMET_ERR_INVALID_ARG;
+  if (!aligned16(X) || (n8 && !aligned16(Xq8)) || (n4 && !aligned16(Xq4)) || !aligned16(Sx) ||
+      (perm && !aligned16(perm)) || (reinterpret_cast<uintptr_t>(scales) & 3))
+    return COMET_ERR_ALIGNMENT;
+  comet_status ds = device_check(nullptr);
+  if (ds != COMET_OK) return ds;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const __half* Xh = reinterpret_cast<const __half*>(X);
+  if (M >= 64 && 2 * K * 2 <= 200 * 1024) {
+    // row-staged kernel (as comet_quantize_act), static-scale arithmetic
+    const int smem = 2 * K * 2;
+    cudaError_t e = cudaFuncSetAttribute(perm ? quantize_act_rows_kernel<true, true> : quantize_act_rows_kernel<false, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return cuda_fail(e);
+    int per_sm = (228 * 1024) / (smem + 1024);
+    if (per_sm > 8) per_sm = 8;
+    if (per_sm < 1) per_sm = 1;
+    int num_sms = 148;
+    device_check(&num_sms);
+    int64_t g = (int64_t)num_sms * per_sm;
+    if (g > ldsx) g = ldsx;
+    if (perm)
+      quantize_act_rows_kernel<true, true><<<(int)g, 256, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8,
+                                                                      (int64_t)n8 * 128, reinterpret_cast<uint8_t*>(Xq4),
+                                                                      (int64_t)n4 * 64, Sx, scales);
+    else
+      quantize_act_rows_kernel<false, true><<<(int)g, 256, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8,
+                                                                       (int64_t)n8 * 128, reinterpret_cast<uint8_t*>(Xq4),
+                                                                       (int64_t)n4 * 64, Sx, scales);
+    return check_launch();
+  }
+  const dim3 grid((unsigned)((ldsx + 7) / 8), (unsigned)((K / 128 + 1) / 2));
+  if (perm)
+    quantize_act_static_kernel<true><<<grid, 256, 0, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, scales, Xq8,
+                                                            (int64_t)n8 * 128, reinterpret_cast<uint8_t*>(Xq4),
+                                                            (int64_t)n4 * 64, Sx);
+  else
+    quantize_act_static_kernel<false><<<grid, 256, 0, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, scales, Xq8,
+                                                             (int64_t)n8 * 128, reinterpret_cast<uint8_t*>(Xq4),
+                                                             (int64_t)n4 * 64, Sx);
+  return check_launch();
+}
+
 comet_status comet_fmpq_map(const float* score, int32_t K, float theta, int32_t* perm, uint8_t* block_bits,
                             int32_t* n_outliers) {
   if (!score || !perm || !block_bits || K <= 0 || !(theta > 1.0f)) return COMET_ERR_INVALID_ARG;

@@ -157,4 +157,73 @@ __global__ void __launch_bounds__(256) kv4_dequantize_kernel(const uint8_t* __re
   }
 }
 
+// f4: static per-block activation scales:
+// scale[b] = fp32(pool_b / qmax_b), pool_b = max of the calibration maxabs over
+// the block's channels on the permuted axis, 1 if pool_b == 0.  CTA = block.
+__global__ void __launch_bounds__(128) static_act_scales_kernel(const float* __restrict__ maxabs,
+                                                                const int32_t* __restrict__ perm,
+                                                                const __grid_constant__ BlockMap map,
+                                                                float* __restrict__ scales) {
+  __shared__ float red[4];
+  const int b = blockIdx.x, i = b * 128 + threadIdx.x;
+  float a = __ldg(maxabs + (perm ? __ldg(perm + i) : i));
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, off));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const float pool = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+    const float qmax = (map.code[b] >> 15) ? 127.0f : 7.0f;
+    scales[b] = pool == 0.0f ? 1.0f : __fdiv_rn(pool, qmax);
+  }
+}
+
+// f4: activation quantize + pack with static per-block scales:
+// q = clamp(rha(fp32(x / scale[b])), -qmax, qmax), Sx[b, m] = scale[b] (so
+// the GEMM is unchanged).  Same grid and plane layout as quantize_act_kernel
+// (half-warp per (row, block) item, lane = 8 channels), no absmax reduction.
+template <bool kPerm>
+__global__ void __launch_bounds__(256) quantize_act_static_kernel(const __half* __restrict__ X, int64_t ldx, int M,
+                                                                  int nb, int64_t ldsx, const int32_t* __restrict__ perm,
+                                                                  const __grid_constant__ BlockMap map,
+                                                                  const float* __restrict__ scales,
+                                                                  int8_t* __restrict__ Xq8, int64_t ld8,
+                                                                  uint8_t* __restrict__ Xq4, int64_t ld4,
+                                                                  float* __restrict__ Sx) {
+  grid_dep_launch();
+  const int half_id = threadIdx.x >> 4;
+  const int o = threadIdx.x & 15;
+  const int64_t m = (int64_t)blockIdx.x * 8 + (half_id & 7);
+  const int b = blockIdx.y * 2 + (half_id >> 3);
+  if (m >= ldsx || b >= nb) return;
+  if (m >= M) {
+    if (o == 0) Sx[(int64_t)b * ldsx + m] = 1.0f;
+    return;
+  }
+  float x[8];
+  load_octet<kPerm>(X, ldx, m, b, o, perm, x);
+  const uint32_t code = map.code[b];
+  const bool is8 = (code >> 15) != 0;
+  const int rank = code & 0x7FFF;
+  const int qmax = is8 ? 127 : 7;
+  const float s = __ldg(scales + b);
+  int32_t q[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float v = __fdiv_rn(x[j], s);
+    // |v| >= 2^23 (incl. inf) is already beyond any qmax: clamp by sign
+    q[j] = fabsf(v) >= 8388608.0f ? (v > 0.0f ? qmax : -qmax) : min(qmax, max(-qmax, round_half_away(v)));
+  }
+  if (is8) {
+    uint32_t lo = (uint32_t)(q[0] & 0xFF) | ((uint32_t)(q[1] & 0xFF) << 8) | ((uint32_t)(q[2] & 0xFF) << 16) |
+                  ((uint32_t)(q[3] & 0xFF) << 24);
+    uint32_t hi = (uint32_t)(q[4] & 0xFF) | ((uint32_t)(q[5] & 0xFF) << 8) | ((uint32_t)(q[6] & 0xFF) << 16) |
+                  ((uint32_t)(q[7] & 0xFF) << 24);
+    *reinterpret_cast<uint2*>(Xq8 + m * ld8 + (int64_t)rank * 128 + o * 8) = make_uint2(lo, hi);
+  } else {
+    *reinterpret_cast<uint32_t*>(Xq4 + m * ld4 + (int64_t)rank * 64 + o * 4) = pack_int4_word(q);
+  }
+  if (o == 0) Sx[(int64_t)b * ldsx + m] = s;
+}
+
 }  // namespace comet

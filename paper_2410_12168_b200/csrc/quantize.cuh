@@ -144,11 +144,15 @@ __global__ void __launch_bounds__(256) quantize_act_kernel(const __half* __restr
 #endif
 // One (row, block) item for the row-staged kernel: `row` is the row in
 // shared memory, `psm` the permutation as u16 in shared memory (kPerm).
-template <bool kPerm>
+// kStatic (f4): the block's scale is the calibrated sstat[b]; q = clamp(rha(
+// fp32(x / s)), -qmax, qmax) (comet_quantize_act_static) instead of the
+// runtime absmax and the reciprocal multiply.
+template <bool kPerm, bool kStatic = false>
 DEVI void quant_item(const unsigned short* row, const unsigned short* psm, const int32_t* __restrict__ gperm,
                      const BlockMap& map, int b, int o,
                      unsigned hmask, int64_t m, int64_t ldsx, int8_t* __restrict__ Xq8, int64_t ld8,
-                     uint8_t* __restrict__ Xq4, int64_t ld4, float* __restrict__ Sx) {
+                     uint8_t* __restrict__ Xq4, int64_t ld4, float* __restrict__ Sx,
+                     const float* __restrict__ sstat = nullptr) {
   const int i0 = b * 128 + o * 8;
   float x[8];
   if (kPerm && !COMET_Q_PERMSMEM) {
@@ -174,22 +178,33 @@ DEVI void quant_item(const unsigned short* row, const unsigned short* psm, const
       x[2 * j + 1] = half_bits_to_float(w[j] >> 16);
     }
   }
-  float a = 0.0f;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) a = fmaxf(a, fabsf(x[j]));
-#pragma unroll
-  for (int off = 8; off >= 1; off >>= 1) a = fmaxf(a, __shfl_xor_sync(hmask, a, off));
   const uint32_t code = map.code[b];
   const bool is8 = (code >> 15) != 0;
   const int rank = code & 0x7FFF;
   const float qmax = is8 ? 127.0f : 7.0f;
-  float s = 1.0f, r = 0.0f;
-  if (a != 0.0f) {
-    s = __fdiv_rn(a, qmax);
-    r = __fdiv_rn(qmax, a);
-  }
+  float s = 1.0f;
   int32_t q[8];
-  quant8(x, r, q);
+  if (kStatic) {
+    s = __ldg(sstat + b);
+    const int qm = is8 ? 127 : 7;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float v = __fdiv_rn(x[j], s);
+      q[j] = fabsf(v) >= 8388608.0f ? (v > 0.0f ? qm : -qm) : min(qm, max(-qm, round_half_away(v)));
+    }
+  } else {
+    float a = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a = fmaxf(a, fabsf(x[j]));
+#pragma unroll
+    for (int off = 8; off >= 1; off >>= 1) a = fmaxf(a, __shfl_xor_sync(hmask, a, off));
+    float r = 0.0f;
+    if (a != 0.0f) {
+      s = __fdiv_rn(a, qmax);
+      r = __fdiv_rn(qmax, a);
+    }
+    quant8(x, r, q);
+  }
   if (is8) {
     uint32_t lo = (uint32_t)(q[0] & 0xFF) | ((uint32_t)(q[1] & 0xFF) << 8) | ((uint32_t)(q[2] & 0xFF) << 16) |
                   ((uint32_t)(q[3] & 0xFF) << 24);
@@ -211,13 +226,14 @@ DEVI void quant_item(const unsigned short* row, const unsigned short* psm, const
 // global loads per lane.  Half-warp per (row, 128-channel block) item, lane =
 // 8 channels, two items in flight per half-warp; arithmetic and output
 // identical to quantize_act_kernel.
-template <bool kPerm>
+template <bool kPerm, bool kStatic = false>
 __global__ void __launch_bounds__(256) quantize_act_rows_kernel(const __half* __restrict__ X, int64_t ldx, int M,
                                                                 int nb, int64_t ldsx, const int32_t* __restrict__ perm,
                                                                 const __grid_constant__ BlockMap map,
                                                                 int8_t* __restrict__ Xq8, int64_t ld8,
                                                                 uint8_t* __restrict__ Xq4, int64_t ld4,
-                                                                float* __restrict__ Sx) {
+                                                                float* __restrict__ Sx,
+                                                                const float* __restrict__ sstat = nullptr) {
   extern __shared__ __align__(16) uint8_t qsm[];
   grid_dep_launch();  // the GEMM that follows may get scheduled (PDL)
   const int K = nb * 128;
@@ -253,10 +269,10 @@ __global__ void __launch_bounds__(256) quantize_act_rows_kernel(const __half* __
     const unsigned short* row = reinterpret_cast<const unsigned short*>(qsm + (size_t)buf * K * 2);
     int b = half_id;
     for (; b + 16 < nb; b += 32) {
-      quant_item<kPerm>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx);
-      quant_item<kPerm>(row, psm, perm, map, b + 16, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx);
+      quant_item<kPerm, kStatic>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat);
+      quant_item<kPerm, kStatic>(row, psm, perm, map, b + 16, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat);
     }
-    if (b < nb) quant_item<kPerm>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx);
+    if (b < nb) quant_item<kPerm, kStatic>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat);
     __syncthreads();  // every half-warp is done with this buffer
   }
 }

@@ -173,7 +173,7 @@ def test_static_planes_through_the_gemm():
     scales_np = O.static_block_scales(np.abs(X.astype(np.float32)).max(axis=0), bits)
     scales = torch.from_numpy(scales_np).to(dev)
     Xq8, Xq4, Sx = comet.comet_quantize_act_static(torch.from_numpy(X).to(dev), bits, scales)
-    Wq, Sw = comet.comet_pack_weight(torch.from_numpy(W).to(dev), bits, 128)
+    Wq, Sw = comet.comet_pack_weight(torch.from_numpy(W).to(dev), None, 128)
     ws = comet.new_workspace(comet.comet_w4ax_gemm_workspace_bytes(M, N, K), dev)
     Y = comet.comet_w4ax_gemm(Xq8, Xq4, Sx, bits, Wq, Sw, 128, workspace=ws).float().cpu().numpy()
     r8, r4, rs = O.quantize_act_static(X, bits, scales_np)

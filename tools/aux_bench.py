@@ -54,6 +54,19 @@ def main():
     t = timed(lambda: comet.comet_dequantize_kv(Q, s, z, 128))
     byts = KV.numel() // 2 + KV.numel() * 2 + 8192 // 128 * 1024 * 5
     out.append({"kernel": "kv4_dequantize", "shape": [8192, 1024, 128], "us": t * 1e6, "GBs": byts / t / 1e9})
+    # f4: static-scale activation quantize vs the dynamic one, M=K=4096, 3/32 INT8 blocks
+    M, K = 4096, 4096
+    bits = np.full(K // 128, 4, np.uint8)
+    bits[:3] = 8
+    Xa = torch.randn(M, K, device="cuda").half()
+    perm = torch.randperm(K, device="cuda").int()
+    sc = comet.comet_static_act_scales(comet.comet_calib_absmax(Xa), bits, perm)
+    planes = comet.alloc_act_planes(M, K, bits, Xa.device)
+    byts = M * K * 2 + M * (3 * 128 + 29 * 64) + (K // 128) * M * 4
+    t = timed(lambda: comet.comet_quantize_act_static(Xa, bits, sc, perm, out=planes))
+    out.append({"kernel": "quantize_act_static", "shape": [M, K], "us": t * 1e6, "GBs": byts / t / 1e9})
+    t = timed(lambda: comet.comet_quantize_act(Xa, bits, perm, out=planes))
+    out.append({"kernel": "quantize_act (dynamic)", "shape": [M, K], "us": t * 1e6, "GBs": byts / t / 1e9})
     for o in out:
         o["frac_of_hbm"] = o["GBs"] / pk
         print(json.dumps(o))
