@@ -90,3 +90,41 @@ def pipelined_linear_allgather(gemm_rows, M: int, per: int, chunks: int, dtype, 
 def chunked_to_full(y_chunks, bounds, N: int) -> torch.Tensor:
     """[P x mc x per] rank-major chunks -> [M x N] (drops the padding)."""
     return torch.cat([gathered_to_full(yc, N) for yc in y_chunks], dim=0)
+
+
+# ----------------------------------- SURVEY 8(f) f4: row-parallel (K) ----
+# The down projection pairs with the N-sharded gate_up: rank r already holds
+# the intermediate activations' channel slice that gate_up produced, so the
+# down GEMM is sharded on its reduction axis K instead -- no all-gather of
+# the intermediate, one reduce-scatter of the output.  Shards are whole
+# 128-channel FMPQ blocks, each rank quantizes its own slice (its blocks'
+# per-(row, block) scales are the ones the unsharded quantizer would compute;
+# the permutation and precision mask are per shard, channels never cross
+# ranks), runs the local W4Ax GEMM to an fp16 partial, and the partials are
+# summed in fp32 by the reduce-scatter over token rows.
+def shard_k(K: int, world: int, rank: int, block: int = 128):
+    """(k0, k1): rank's contiguous K range, whole blocks (may be empty)."""
+    nb = K // block
+    per = -(-nb // world)
+    k0 = min(rank * per, nb) * block
+    return k0, min((rank * per + per), nb) * block
+
+
+def row_parallel_reduce(y_partial: torch.Tensor, group=None, scatter: bool = True) -> torch.Tensor:
+    """Sum the ranks' [M x N] fp16 partials in fp32.  scatter: each rank gets
+    its contiguous block of ceil(M / P) token rows (reduce-scatter; the last
+    rank's block may be short), else the full sum on every rank (all-reduce).
+    Returns fp32."""
+    world = dist.get_world_size(group)
+    M, N = y_partial.shape
+    y32 = y_partial.to(torch.float32)
+    if not scatter:
+        dist.all_reduce(y32, group=group)
+        return y32
+    per = -(-M // world)
+    buf = torch.zeros((per * world, N), dtype=torch.float32, device=y32.device)
+    buf[:M] = y32
+    out = torch.empty((per, N), dtype=torch.float32, device=y32.device)
+    dist.reduce_scatter_tensor(out, buf, group=group)
+    rank = dist.get_rank(group)
+    return out[: max(0, min(per, M - rank * per))]
