@@ -104,6 +104,14 @@ comet_status comet_pack_weight(const void* W, int64_t ldw, int32_t N, int32_t K,
 comet_status comet_quantize_act(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
                                 const uint8_t* block_bits, int8_t* Xq8, void* Xq4, float* Sx, int64_t ldsx,
                                 comet_stream_t stream);
+/* f4 variant ("BF16 activations"): identical to
+ * comet_quantize_act except that X holds bf16 values (same shape, stride and
+ * alignment rules); every bf16 value converts to fp32 exactly, after which
+ * the arithmetic, the planes and Sx are those of comet_quantize_act on the
+ * same fp32 values. */
+comet_status comet_quantize_act_bf16(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
+                                     const uint8_t* block_bits, int8_t* Xq8, void* Xq4, float* Sx, int64_t ldsx,
+                                     comet_stream_t stream);
 
 /* ---- a3..a8: the W4Ax GEMM -------------------------
  * Y[m,n] = sum_b Sx[b,m] * Sw[g(b),n] * sum_{i in block b} xq[m,i]*wq[n,i]

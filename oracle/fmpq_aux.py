@@ -218,3 +218,41 @@ def quantize_act_static(X: np.ndarray, bits, scales: np.ndarray, perm=None, k: i
         else:
             r4 += 1
     return Xq8, Xq4, Sx
+
+
+# f4 variant: bf16 activations.  A bf16 value's bits shifted left by 16 are
+# its fp32 encoding (exact); from there the quantization is O3 (the C
+# oracle's oracle_quantize_block, via oracle.quantize_block) on the permuted
+# row, packed as in oracle.quantize_act.
+def bf16_bits_to_f32(bits16: np.ndarray) -> np.ndarray:
+    return (np.asarray(bits16, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+def quantize_act_bf16(Xbits: np.ndarray, bits, perm=None, k: int = BLOCK):
+    """Xbits uint16 [M x K] (bf16 encodings) -> (Xq8, Xq4, Sx) in the comet layout."""
+    from . import ldsx_for, pack_int4, plane_widths, quantize_block
+
+    X = bf16_bits_to_f32(Xbits)
+    M, K = X.shape
+    nb = K // k
+    order = np.arange(K) if perm is None else np.asarray(perm, dtype=np.int64)
+    Xp = X[:, order]
+    K8, K4 = plane_widths(bits, k)
+    Xq8 = np.zeros((M, K8), np.int8)
+    Xq4 = np.zeros((M, K4 // 2), np.uint8)
+    Sx = np.ones((nb, ldsx_for(M)), np.float32)
+    r8 = r4 = 0
+    for b in range(nb):
+        is8 = int(bits[b]) == 8
+        for m in range(M):
+            q, s = quantize_block(Xp[m, b * k:(b + 1) * k], 127 if is8 else 7)
+            if is8:
+                Xq8[m, r8 * k:(r8 + 1) * k] = q
+            else:
+                Xq4[m, r4 * k // 2:(r4 + 1) * k // 2] = pack_int4(q)
+            Sx[b, m] = s
+        if is8:
+            r8 += 1
+        else:
+            r4 += 1
+    return Xq8, Xq4, Sx

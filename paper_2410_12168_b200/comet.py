@@ -25,6 +25,7 @@ EXPORTS = ["comet_act_plane8_bytes", "comet_act_plane4_bytes", "comet_act_ldsx",
            "comet_w4ax_linear_scratch_bytes", "comet_pack_weight", "comet_quantize_act", "comet_w4ax_gemm",
            "comet_w4ax_gemm_acc_i32", "comet_w4ax_linear", "comet_calib_absmax", "comet_fmpq_map",
            "comet_quantize_kv", "comet_dequantize_kv", "comet_static_act_scales", "comet_quantize_act_static",
+           "comet_quantize_act_bf16",
            "comet_status_str", "comet_last_cuda_error",
            "comet_launch_count"]
 
@@ -78,6 +79,8 @@ def lib():
         L.comet_quantize_kv.restype = ctypes.c_int
         L.comet_dequantize_kv.argtypes = [P, P, P, i32, i32, i32, P, i64, P]
         L.comet_dequantize_kv.restype = ctypes.c_int
+        L.comet_quantize_act_bf16.argtypes = [P, i64, i32, i32, P, P, P, P, P, i64, P]
+        L.comet_quantize_act_bf16.restype = ctypes.c_int
         L.comet_static_act_scales.argtypes = [P, i32, P, P, P, P]
         L.comet_static_act_scales.restype = ctypes.c_int
         L.comet_quantize_act_static.argtypes = [P, i64, i32, i32, P, P, P, P, P, P, i64, P]
@@ -220,6 +223,18 @@ def comet_quantize_act_static(X: torch.Tensor, bits, scales: torch.Tensor, perm:
                                          _ptr(Xq8) if b.n8 else None, _ptr(Xq4) if b.n4 else None, _ptr(Sx),
                                          Sx.shape[1], _stream(stream))
     _check("comet_quantize_act_static", st)
+    return Xq8, Xq4, Sx
+
+
+def comet_quantize_act_bf16(X: torch.Tensor, bits, perm: Optional[torch.Tensor] = None, out=None, stream=None):
+    """f4: comet_quantize_act for bf16 activations X [M x K]."""
+    assert X.is_cuda and X.dtype == torch.bfloat16 and X.dim() == 2 and X.stride(1) == 1
+    b = as_bits(bits)
+    M, K = X.shape
+    Xq8, Xq4, Sx = out if out is not None else alloc_act_planes(M, K, b, X.device)
+    st = lib().comet_quantize_act_bf16(_ptr(X), X.stride(0), M, K, _ptr(perm), b.ptr, _ptr(Xq8) if b.n8 else None,
+                                       _ptr(Xq4) if b.n4 else None, _ptr(Sx), Sx.shape[1], _stream(stream))
+    _check("comet_quantize_act_bf16", st)
     return Xq8, Xq4, Sx
 
 

@@ -419,6 +419,61 @@ int64_t plane_bytes(int32_t M, int32_t K, const uint8_t* bits, int want) {
 
 int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
 
+template <bool kBf16>
+comet_status quantize_act_impl(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
+                               const uint8_t* block_bits, int8_t* Xq8, void* Xq4, float* Sx, int64_t ldsx,
+                               comet_stream_t stream) {
+  if (M < 0 || K <= 0 || !block_bits) return COMET_ERR_INVALID_ARG;
+  if (K % 128 || K > 65536 || ldx < K || ldx % 8 || ldsx < M || ldsx % 4) return COMET_ERR_SHAPE;
+  BlockMap map;
+  int n8 = 0, n4 = 0;
+  if (!build_block_map(block_bits, K / 128, &map, &n8, &n4)) return COMET_ERR_INVALID_ARG;
+  if (M == 0) return COMET_OK;
+  if (!X || !Sx || (n8 && !Xq8) || (n4 && !Xq4)) return COMET_ERR_INVALID_ARG;
+  if (!aligned16(X) || (n8 && !aligned16(Xq8)) || (n4 && !aligned16(Xq4)) || !aligned16(Sx) ||
+      (perm && !aligned16(perm)))
+    return COMET_ERR_ALIGNMENT;
+  int num_sms = 148;
+  comet_status ds = device_check(&num_sms);
+  if (ds != COMET_OK) return ds;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const __half* Xh = reinterpret_cast<const __half*>(X);
+  if (M >= 64) {
+    // row-staged kernel: persistent CTAs, double-buffered rows in smem
+    const int smem = 2 * K * 2 + ((perm && COMET_Q_PERMSMEM) ? K * 2 : 0);  // two row buffers + u16 permutation
+    if (smem <= 200 * 1024) {
+      // (dynamic smem above the 48 KB default needs the opt-in; set per call,
+      // it is a cheap host-side attribute)
+      cudaError_t e = cudaFuncSetAttribute(perm ? quantize_act_rows_kernel<true, false, kBf16> : quantize_act_rows_kernel<false, false, kBf16>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return cuda_fail(e);
+      int per_sm = (228 * 1024) / (smem + 1024);
+      if (per_sm > 8) per_sm = 8;
+      if (per_sm < 1) per_sm = 1;
+      int64_t grid = (int64_t)num_sms * per_sm;
+      if (grid > ldsx) grid = ldsx;
+      if (perm)
+        quantize_act_rows_kernel<true, false, kBf16><<<(int)grid, 256, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8,
+                                                                      (int64_t)n8 * 128, reinterpret_cast<uint8_t*>(Xq4),
+                                                                      (int64_t)n4 * 64, Sx);
+      else
+        quantize_act_rows_kernel<false, false, kBf16><<<(int)grid, 256, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8,
+                                                                       (int64_t)n8 * 128, reinterpret_cast<uint8_t*>(Xq4),
+                                                                       (int64_t)n4 * 64, Sx);
+      return check_launch();
+    }
+  }
+  // one CTA per (8 rows, 2 blocks): 16 half-warp items
+  const dim3 grid((unsigned)((ldsx + 7) / 8), (unsigned)((K / 128 + 1) / 2));
+  if (perm)
+    quantize_act_kernel<true, false, kBf16><<<grid, 256, 0, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
+                                                          reinterpret_cast<uint8_t*>(Xq4), (int64_t)n4 * 64, Sx);
+  else
+    quantize_act_kernel<false, false, kBf16><<<grid, 256, 0, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
+                                                           reinterpret_cast<uint8_t*>(Xq4), (int64_t)n4 * 64, Sx);
+  return check_launch();
+}
+
 }  // namespace
 
 extern "C" {
@@ -480,55 +535,13 @@ comet_status comet_pack_weight(const void* W, int64_t ldw, int32_t N, int32_t K,
 comet_status comet_quantize_act(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
                                 const uint8_t* block_bits, int8_t* Xq8, void* Xq4, float* Sx, int64_t ldsx,
                                 comet_stream_t stream) {
-  if (M < 0 || K <= 0 || !block_bits) return COMET_ERR_INVALID_ARG;
-  if (K % 128 || K > 65536 || ldx < K || ldx % 8 || ldsx < M || ldsx % 4) return COMET_ERR_SHAPE;
-  BlockMap map;
-  int n8 = 0, n4 = 0;
-  if (!build_block_map(block_bits, K / 128, &map, &n8, &n4)) return COMET_ERR_INVALID_ARG;
-  if (M == 0) return COMET_OK;
-  if (!X || !Sx || (n8 && !Xq8) || (n4 && !Xq4)) return COMET_ERR_INVALID_ARG;
-  if (!aligned16(X) || (n8 && !aligned16(Xq8)) || (n4 && !aligned16(Xq4)) || !aligned16(Sx) ||
-      (perm && !aligned16(perm)))
-    return COMET_ERR_ALIGNMENT;
-  int num_sms = 148;
-  comet_status ds = device_check(&num_sms);
-  if (ds != COMET_OK) return ds;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const __half* Xh = reinterpret_cast<const __half*>(X);
-  if (M >= 64) {
-    // row-staged kernel: persistent CTAs, double-buffered rows in smem
-    const int smem = 2 * K * 2 + ((perm && COMET_Q_PERMSMEM) ? K * 2 : 0);  // two row buffers + u16 permutation
-    if (smem <= 200 * 1024) {
-      // (dynamic smem above the 48 KB default needs the opt-in; set per call,
-      // it is a cheap host-side attribute)
-      cudaError_t e = cudaFuncSetAttribute(perm ? quantize_act_rows_kernel<true> : quantize_act_rows_kernel<false>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return cuda_fail(e);
-      int per_sm = (228 * 1024) / (smem + 1024);
-      if (per_sm > 8) per_sm = 8;
-      if (per_sm < 1) per_sm = 1;
-      int64_t grid = (int64_t)num_sms * per_sm;
-      if (grid > ldsx) grid = ldsx;
-      if (perm)
-        quantize_act_rows_kernel<true><<<(int)grid, 256, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8,
-                                                                      (int64_t)n8 * 128, reinterpret_cast<uint8_t*>(Xq4),
-                                                                      (int64_t)n4 * 64, Sx);
-      else
-        quantize_act_rows_kernel<false><<<(int)grid, 256, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8,
-                                                                       (int64_t)n8 * 128, reinterpret_cast<uint8_t*>(Xq4),
-                                                                       (int64_t)n4 * 64, Sx);
-      return check_launch();
-    }
-  }
-  // one CTA per (8 rows, 2 blocks): 16 half-warp items
-  const dim3 grid((unsigned)((ldsx + 7) / 8), (unsigned)((K / 128 + 1) / 2));
-  if (perm)
-    quantize_act_kernel<true><<<grid, 256, 0, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
-                                                          reinterpret_cast<uint8_t*>(Xq4), (int64_t)n4 * 64, Sx);
-  else
-    quantize_act_kernel<false><<<grid, 256, 0, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
-                                                           reinterpret_cast<uint8_t*>(Xq4), (int64_t)n4 * 64, Sx);
-  return check_launch();
+  return quantize_act_impl<false>(X, ldx, M, K, perm, block_bits, Xq8, Xq4, Sx, ldsx, stream);
+}
+
+comet_status comet_quantize_act_bf16(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
+                                     const uint8_t* block_bits, int8_t* Xq8, void* Xq4, float* Sx, int64_t ldsx,
+                                     comet_stream_t stream) {
+  return quantize_act_impl<true>(X, ldx, M, K, perm, block_bits, Xq8, Xq4, Sx, ldsx, stream);
 }
 
 comet_status comet_w4ax_gemm(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,

@@ -22,6 +22,11 @@ struct BlockMap {
 };
 
 DEVI float half_bits_to_float(uint32_t h) { return __half2float(__ushort_as_half((unsigned short)h)); }
+// activation element bits -> fp32 (exact for both): fp16, or bf16 (f4 variant)
+template <bool kBf16>
+DEVI float act_bits_to_float(uint32_t h) {
+  return kBf16 ? __uint_as_float((h & 0xFFFFu) << 16) : half_bits_to_float(h);
+}
 
 // round half away from zero of v, exact for |v| < 2^23:
 // floor(RZ(|v| + 0.5)) == floor(|v| + 0.5) because RZ never crosses the
@@ -46,7 +51,7 @@ DEVI uint32_t pack_int4_word(const int32_t (&q)[8]) {
 
 // Load the lane's 8 channels of row m, block b (positions 128b + 8*o .. +7
 // on the permuted axis).
-template <bool kPerm>
+template <bool kPerm, bool kBf16 = false>
 DEVI void load_octet(const __half* __restrict__ X, int64_t ldx, int64_t m, int b, int o, const int32_t* __restrict__ perm,
                      float (&x)[8]) {
   const int i0 = b * 128 + o * 8;
@@ -55,8 +60,8 @@ DEVI void load_octet(const __half* __restrict__ X, int64_t ldx, int64_t m, int b
     uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      x[2 * j] = half_bits_to_float(w[j] & 0xFFFF);
-      x[2 * j + 1] = half_bits_to_float(w[j] >> 16);
+      x[2 * j] = act_bits_to_float<kBf16>(w[j] & 0xFFFF);
+      x[2 * j + 1] = act_bits_to_float<kBf16>(w[j] >> 16);
     }
   } else {
     int4 p0 = __ldg(reinterpret_cast<const int4*>(perm + i0));
@@ -64,7 +69,7 @@ DEVI void load_octet(const __half* __restrict__ X, int64_t ldx, int64_t m, int b
     int p[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
     const unsigned short* row = reinterpret_cast<const unsigned short*>(X + m * ldx);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) x[j] = half_bits_to_float(__ldg(row + p[j]));
+    for (int j = 0; j < 8; ++j) x[j] = act_bits_to_float<kBf16>(__ldg(row + p[j]));
   }
 }
 
@@ -83,7 +88,7 @@ DEVI int64_t wq_tiled_offset(int64_t n, int64_t p, int nb) {
 // blocks; half-warp h of the CTA takes row 8x + (h & 7) of block 2y + (h >> 3)
 // (no 64-bit index arithmetic: the previous grid-stride form spent more
 // instructions on 64-bit item division than on the quantization).
-template <bool kPerm, bool kTiledW = false>
+template <bool kPerm, bool kTiledW = false, bool kBf16 = false>
 __global__ void __launch_bounds__(256) quantize_act_kernel(const __half* __restrict__ X, int64_t ldx, int M, int nb,
                                                            int64_t ldsx, const int32_t* __restrict__ perm,
                                                            const __grid_constant__ BlockMap map, int8_t* __restrict__ Xq8,
@@ -101,7 +106,7 @@ __global__ void __launch_bounds__(256) quantize_act_kernel(const __half* __restr
     return;
   }
   float x[8];
-  load_octet<kPerm>(X, ldx, m, b, o, perm, x);
+  load_octet<kPerm, kBf16>(X, ldx, m, b, o, perm, x);
   float a = 0.0f;
 #pragma unroll
   for (int j = 0; j < 8; ++j) a = fmaxf(a, fabsf(x[j]));
@@ -132,13 +137,6 @@ __global__ void __launch_bounds__(256) quantize_act_kernel(const __half* __restr
   if (o == 0) Sx[(int64_t)b * ldsx + m] = s;
 }
 
-// Activation quantize + pack, row-staged variant (a1 + a2 for the GEMM
-// path): persistent CTAs walk rows; each row (K fp16, contiguous) arrives in
-// shared memory by one 1-D bulk copy (the next row's copy is in flight while
-// this one is quantized), and the fused channel gather reads the
-// permuted positions from shared memory instead of issuing 8 scattered 2-byte
-// global loads per lane.  Half-warp per (row, 128-channel block) item, lane =
-// 8 channels, as in quantize_act_kernel (identical arithmetic and output).
 #ifndef COMET_Q_PERMSMEM
 #define COMET_Q_PERMSMEM 0  // 1: permutation cached in shared memory as u16 (measured slower: occupancy)
 #endif
@@ -147,7 +145,7 @@ __global__ void __launch_bounds__(256) quantize_act_kernel(const __half* __restr
 // kStatic (f4): the block's scale is the calibrated sstat[b]; q = clamp(rha(
 // fp32(x / s)), -qmax, qmax) (comet_quantize_act_static) instead of the
 // runtime absmax and the reciprocal multiply.
-template <bool kPerm, bool kStatic = false>
+template <bool kPerm, bool kStatic = false, bool kBf16 = false>
 DEVI void quant_item(const unsigned short* row, const unsigned short* psm, const int32_t* __restrict__ gperm,
                      const BlockMap& map, int b, int o,
                      unsigned hmask, int64_t m, int64_t ldsx, int8_t* __restrict__ Xq8, int64_t ld8,
@@ -160,22 +158,22 @@ DEVI void quant_item(const unsigned short* row, const unsigned short* psm, const
     const int4 p1 = __ldg(reinterpret_cast<const int4*>(gperm + i0 + 4));
     const int p[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
 #pragma unroll
-    for (int j = 0; j < 8; ++j) x[j] = half_bits_to_float(row[p[j]]);
+    for (int j = 0; j < 8; ++j) x[j] = act_bits_to_float<kBf16>(row[p[j]]);
   } else if (kPerm) {
     const uint4 pv = *reinterpret_cast<const uint4*>(psm + i0);  // 8 x u16 source positions
     const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      x[2 * j] = half_bits_to_float(row[pw[j] & 0xFFFF]);
-      x[2 * j + 1] = half_bits_to_float(row[pw[j] >> 16]);
+      x[2 * j] = act_bits_to_float<kBf16>(row[pw[j] & 0xFFFF]);
+      x[2 * j + 1] = act_bits_to_float<kBf16>(row[pw[j] >> 16]);
     }
   } else {
     const uint4 v = *reinterpret_cast<const uint4*>(row + i0);
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      x[2 * j] = half_bits_to_float(w[j] & 0xFFFF);
-      x[2 * j + 1] = half_bits_to_float(w[j] >> 16);
+      x[2 * j] = act_bits_to_float<kBf16>(w[j] & 0xFFFF);
+      x[2 * j + 1] = act_bits_to_float<kBf16>(w[j] >> 16);
     }
   }
   const uint32_t code = map.code[b];
@@ -226,7 +224,7 @@ DEVI void quant_item(const unsigned short* row, const unsigned short* psm, const
 // global loads per lane.  Half-warp per (row, 128-channel block) item, lane =
 // 8 channels, two items in flight per half-warp; arithmetic and output
 // identical to quantize_act_kernel.
-template <bool kPerm, bool kStatic = false>
+template <bool kPerm, bool kStatic = false, bool kBf16 = false>
 __global__ void __launch_bounds__(256) quantize_act_rows_kernel(const __half* __restrict__ X, int64_t ldx, int M,
                                                                 int nb, int64_t ldsx, const int32_t* __restrict__ perm,
                                                                 const __grid_constant__ BlockMap map,
@@ -269,10 +267,10 @@ __global__ void __launch_bounds__(256) quantize_act_rows_kernel(const __half* __
     const unsigned short* row = reinterpret_cast<const unsigned short*>(qsm + (size_t)buf * K * 2);
     int b = half_id;
     for (; b + 16 < nb; b += 32) {
-      quant_item<kPerm, kStatic>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat);
-      quant_item<kPerm, kStatic>(row, psm, perm, map, b + 16, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat);
+      quant_item<kPerm, kStatic, kBf16>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat);
+      quant_item<kPerm, kStatic, kBf16>(row, psm, perm, map, b + 16, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat);
     }
-    if (b < nb) quant_item<kPerm, kStatic>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat);
+    if (b < nb) quant_item<kPerm, kStatic, kBf16>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat);
     __syncthreads();  // every half-warp is done with this buffer
   }
 }
