@@ -440,7 +440,7 @@ comet_status quantize_act_impl(const void* X, int64_t ldx, int32_t M, int32_t K,
   const __half* Xh = reinterpret_cast<const __half*>(X);
   if (M >= 64) {
     // row-staged kernel: persistent CTAs, double-buffered rows in smem
-    const int smem = 2 * K * 2 + ((perm && COMET_Q_PERMSMEM) ? K * 2 : 0);  // two row buffers + u16 permutation
+    const int smem = kQNBuf * K * 2 + ((perm && COMET_Q_PERMSMEM) ? K * 2 : 0);  // row buffers + u16 permutation
     if (smem <= 200 * 1024) {
       // (dynamic smem above the 48 KB default needs the opt-in; set per call,
       // it is a cheap host-side attribute)
@@ -693,9 +693,9 @@ comet_status comet_quantize_act_static(const void* X, int64_t ldx, int32_t M, in
   if (ds != COMET_OK) return ds;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const __half* Xh = reinterpret_cast<const __half*>(X);
-  if (M >= 64 && 2 * K * 2 <= 200 * 1024) {
+  if (M >= 64 && kQNBuf * K * 2 <= 200 * 1024) {
     // row-staged kernel (as comet_quantize_act), static-scale arithmetic
-    const int smem = 2 * K * 2;
+    const int smem = kQNBuf * K * 2;
     cudaError_t e = cudaFuncSetAttribute(perm ? quantize_act_rows_kernel<true, true> : quantize_act_rows_kernel<false, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_fail(e);

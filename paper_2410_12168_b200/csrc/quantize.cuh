@@ -137,6 +137,10 @@ __global__ void __launch_bounds__(256) quantize_act_kernel(const __half* __restr
   if (o == 0) Sx[(int64_t)b * ldsx + m] = s;
 }
 
+#ifndef COMET_Q_NBUF
+#define COMET_Q_NBUF 2  // row buffers per CTA (rows in flight = COMET_Q_NBUF - 1 ahead)
+#endif
+constexpr int kQNBuf = COMET_Q_NBUF;
 #ifndef COMET_Q_PERMSMEM
 #define COMET_Q_PERMSMEM 0  // 1: permutation cached in shared memory as u16 (measured slower: occupancy)
 #endif
@@ -235,14 +239,13 @@ __global__ void __launch_bounds__(256) quantize_act_rows_kernel(const __half* __
   extern __shared__ __align__(16) uint8_t qsm[];
   grid_dep_launch();  // the GEMM that follows may get scheduled (PDL)
   const int K = nb * 128;
-  __shared__ uint64_t rbar[2];
+  __shared__ uint64_t rbar[kQNBuf];
   const int half_id = threadIdx.x >> 4;
   const int o = threadIdx.x & 15;
   const unsigned hmask = 0xFFFFu << (threadIdx.x & 16);
-  unsigned short* psm = reinterpret_cast<unsigned short*>(qsm + (size_t)4 * K);
+  unsigned short* psm = reinterpret_cast<unsigned short*>(qsm + (size_t)kQNBuf * 2 * K);
   if (threadIdx.x == 0) {
-    mbar_init(&rbar[0], 1);
-    mbar_init(&rbar[1], 1);
+    for (int i = 0; i < kQNBuf; ++i) mbar_init(&rbar[i], 1);
     fence_mbar_init();
   }
   if (kPerm && COMET_Q_PERMSMEM)
@@ -253,17 +256,21 @@ __global__ void __launch_bounds__(256) quantize_act_rows_kernel(const __half* __
     bulk_load(qsm + (size_t)buf * K * 2, X + m * ldx, (uint32_t)K * 2, &rbar[buf]);
   };
   int64_t m = blockIdx.x;
-  if (threadIdx.x == 0 && m < M) issue(m, 0);
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kQNBuf - 1; ++i)
+      if (m + (int64_t)i * gridDim.x < M) issue(m + (int64_t)i * gridDim.x, i);
   for (int it = 0; m < ldsx; ++it, m += gridDim.x) {
-    const int buf = it & 1;
+    const int buf = it % kQNBuf;
     if (m >= M) {  // padding rows of the scale layout
       for (int b = threadIdx.x; b < nb; b += blockDim.x) Sx[(int64_t)b * ldsx + m] = 1.0f;
       continue;
     }
-    // prefetch the next row into the other buffer (its previous contents
-    // were consumed before the __syncthreads that ended the last iteration)
-    if (threadIdx.x == 0 && m + gridDim.x < M) issue(m + gridDim.x, buf ^ 1);
-    mbar_wait(&rbar[buf], (it >> 1) & 1);
+    // prefetch row it + kQNBuf - 1 into the buffer row it - 1 used (its
+    // contents were consumed before the __syncthreads that ended the last
+    // iteration)
+    const int64_t mp = m + (int64_t)(kQNBuf - 1) * gridDim.x;
+    if (threadIdx.x == 0 && mp < M) issue(mp, (it + kQNBuf - 1) % kQNBuf);
+    mbar_wait(&rbar[buf], (it / kQNBuf) & 1);
     const unsigned short* row = reinterpret_cast<const unsigned short*>(qsm + (size_t)buf * K * 2);
     int b = half_id;
     for (; b + 16 < nb; b += 32) {
