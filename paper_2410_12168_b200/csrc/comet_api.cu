@@ -354,7 +354,10 @@ comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, in
     return COMET_ERR_CUDA;
   if (n4 && PfCfg::kXPre && p.two_sm && use_pf()) {
     // pre-expanded INT4 token blocks (x16 INT8, staging byte order) in a
-    // cached device buffer, TMA-loaded as SW128 INT8 rows like the INT8 plane
+    // cached device buffer, TMA-loaded as SW128 INT8 rows like the INT8 plane.
+    // EXPERIMENT ONLY (COMET_PF_XPRE, off by default): the process-wide buffer
+    // is neither thread- nor multi-stream-safe; a product version would take
+    // it from the caller's workspace
     static void* xe = nullptr;
     static size_t xe_bytes = 0;
     const size_t need = (size_t)M * n4 * 128;
