@@ -246,8 +246,10 @@ def run_comet(args, cfg, config_name):
         Xh = torch.from_numpy(p["X"]).pin_memory()
         Yh = torch.empty((M, per), dtype=torch.float16).pin_memory()
         scratch = comet.new_workspace(comet.comet_w4ax_linear_scratch_bytes(M, per, K, bits), dev)
-        layers.append(dict(N=N, K=K, grp=grp, per=per, W=W, perm=perm, bits=bits, Wq=Wq, Sw=Sw, X=X, planes=planes, Y=Y,
-                           ws=ws, Yall=Yall, Xh=Xh, Yh=Yh, scratch=scratch, ev=[], qev=[]))
+        # --expanded-weights: the prefill kernel reads an offline INT8 copy (a4 done once)
+        We = comet.comet_expand_weight(Wq) if args.expanded_weights else None
+        layers.append(dict(N=N, K=K, grp=grp, per=per, W=W, perm=perm, bits=bits, Wq=Wq, We=We, Sw=Sw, X=X,
+                           planes=planes, Y=Y, ws=ws, Yall=Yall, Xh=Xh, Yh=Yh, scratch=scratch, ev=[], qev=[]))
         del p
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
@@ -260,7 +262,8 @@ def run_comet(args, cfg, config_name):
 
             def gemm_rows(m0, m1, out, L=L):
                 Xq8, Xq4, Sx = comet.comet_quantize_act(L["X"][m0:m1], L["bits"], L["perm"], out=L["cplanes"][(m0, m1)])
-                comet.comet_w4ax_gemm(Xq8, Xq4, Sx, L["bits"], L["Wq"], L["Sw"], L["grp"], out=out, workspace=L["ws"])
+                comet.comet_w4ax_gemm_ex(Xq8, Xq4, Sx, L["bits"], L["Wq"], L["We"], L["Sw"], L["grp"], out=out,
+                                         workspace=L["ws"])
             L["gemm_rows"] = gemm_rows
 
     def step(timed_kernels=False):
@@ -285,7 +288,8 @@ def run_comet(args, cfg, config_name):
                 L["qev"].append((qa, qb))
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-            comet.comet_w4ax_gemm(Xq8, Xq4, Sx, L["bits"], L["Wq"], L["Sw"], L["grp"], out=L["Y"], workspace=L["ws"])
+            comet.comet_w4ax_gemm_ex(Xq8, Xq4, Sx, L["bits"], L["Wq"], L["We"], L["Sw"], L["grp"], out=L["Y"],
+                                     workspace=L["ws"])
             if timed_kernels:
                 b.record(stream)
                 L["ev"].append((a, b))
@@ -396,6 +400,7 @@ def run_comet(args, cfg, config_name):
            "vs_baseline": None, "dtype": "int8 (INT4/INT8 operands) x int32 accum, fp32 dequant, fp16 out",
            "data": "synthetic (seeded; X~N(0,1) + planted outlier channels, W~N(0,1/K))",
            "config": {"workload": cfg["workload"], "M": M, "layers": cfg["layers"], "weight_scales": args.group,
+                      "weights": "INT4 + offline INT8 copy for prefill" if args.expanded_weights else "INT4 packed",
                       "parallelism": (f"tp{world} (N-sharded, NCCL all-gather of Y"
                                       + (f", {chunks} row chunks pipelining GEMM and all-gather)" if chunks > 1 else ")")
                                       if world > 1 else "single GPU"),
@@ -440,6 +445,8 @@ def main():
     ap.add_argument("--group", default="channel", choices=["channel", "128"],
                     help="weight-scale granularity: per output channel (OmniQuant W4A4 style, default) or 128-groups")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--expanded-weights", action="store_true",
+                    help="prefill GEMM reads an offline INT8 copy of the weights (comet_expand_weight): 2x weight memory")
     ap.add_argument("--overlap-chunks", type=int, default=0,
                     help="N > 1: row chunks pipelining GEMM and all-gather (0: auto = 4 for M >= 1024, 1: serial)")
     args = ap.parse_args()

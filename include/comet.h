@@ -126,6 +126,23 @@ comet_status comet_w4ax_gemm(const int8_t* Xq8, const void* Xq4, const float* Sx
                              int32_t N, int32_t group, void* Y, int64_t ldy, void* workspace,
                              size_t workspace_bytes, comet_stream_t stream);
 
+/* ---- a4 done offline: pre-expanded weights for the prefill kernel --------
+ * comet_expand_weight: We int8 [N x K] (DEVICE, row-major, N*K bytes) with
+ *   We[n, k] = 16 * wq[n, k] -- the zero-extension of P:L294 applied once
+ *   to the packed weights of comet_pack_weight (Wq, tiled layout) instead of
+ *   in every prefill GEMM (twice the weight bytes: a memory-for-speed
+ *   option for prefill-heavy layers).
+ * comet_w4ax_gemm_ex: comet_w4ax_gemm with the expanded copy: for M > 128
+ *   the prefill kernel TMA-loads We straight into its weight operand (no
+ *   in-kernel weight expansion); for M <= 128 (HBM-bound decode) it reads the
+ *   packed Wq.  Wq is always required, We may be NULL (= comet_w4ax_gemm);
+ *   results are identical to comet_w4ax_gemm. */
+comet_status comet_expand_weight(const void* Wq, int32_t N, int32_t K, void* We, comet_stream_t stream);
+comet_status comet_w4ax_gemm_ex(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
+                                const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq, const void* We,
+                                const float* Sw, int32_t N, int32_t group, void* Y, int64_t ldy, void* workspace,
+                                size_t workspace_bytes, comet_stream_t stream);
+
 /* ---- test/debug: per-block INT32 accumulators ---------------------------
  * Acc int32 [K/128 x M x N]: Acc[(b*M + m)*N + n] = sum_{i in block b}
  * xq[m,i]*wq[n,i] in LOGICAL units (the x16 / x256 zero-extension factors

@@ -218,11 +218,11 @@ comet_status launch_gemm_2sm(const CUtensorMap& tmW, const CUtensorMap& tmX4, co
   return check_launch();
 }
 
-template <bool kGroupK, bool kAcc>
+template <bool kGroupK, bool kAcc, bool kXW = false>
 comet_status launch_gemm_pf(const CUtensorMap& tmX4, const CUtensorMap& tmX8, const BlockMap& map,
-                            const GemmArgs& args, const Plan& p, cudaStream_t st) {
+                            const GemmArgs& args, const Plan& p, cudaStream_t st, const void* We = nullptr) {
   using C = PfCfg;
-  auto kern = w4ax_gemm_pf_kernel<kGroupK, kAcc>;
+  auto kern = w4ax_gemm_pf_kernel<kGroupK, kAcc, kXW>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes); });
@@ -240,7 +240,11 @@ comet_status launch_gemm_pf(const CUtensorMap& tmX4, const CUtensorMap& tmX8, co
   // plain launch: PDL overlap with the quantizer measured ~1% slower for the
   // prefill kernel (the decode kernel, whose weight stream can start early,
   // gains 4-16%); griddepcontrol.wait is a no-op without the attribute
-  kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(tmY, tmX4, tmX8, map, args, sched);
+  CUtensorMap tmWE = tmX4;  // dereferenced only with expanded weights (kXW)
+  if (kXW && !make_map_u8(&tmWE, We, (uint64_t)args.K, (uint64_t)args.N, (uint64_t)args.K, 128, C::kRows,
+                          CU_TENSOR_MAP_SWIZZLE_128B))
+    return COMET_ERR_CUDA;
+  kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(tmY, tmX4, tmX8, tmWE, map, args, sched);
   return check_launch();
 }
 
@@ -307,8 +311,13 @@ bool use_pf() {
 
 template <bool kAcc>
 comet_status launch_gemm(const CUtensorMap& tmW, const CUtensorMap& tmX4, const CUtensorMap& tmX8,
-                         const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
+                         const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st,
+                         const void* We = nullptr) {
   const bool group_k = args.group_blocks == args.nb;
+  if (p.two_sm && use_pf() && We) {
+    if (group_k) return launch_gemm_pf<true, kAcc, true>(tmX4, tmX8, map, args, p, st, We);
+    return launch_gemm_pf<false, kAcc, true>(tmX4, tmX8, map, args, p, st, We);
+  }
   if (p.two_sm && use_pf()) {
     if (group_k) return launch_gemm_pf<true, kAcc>(tmX4, tmX8, map, args, p, st);
     return launch_gemm_pf<false, kAcc>(tmX4, tmX8, map, args, p, st);
@@ -323,7 +332,8 @@ comet_status launch_gemm(const CUtensorMap& tmW, const CUtensorMap& tmX4, const 
 
 comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx, const uint8_t* bits,
                          int32_t M, int32_t K, const void* Wq, const float* Sw, int32_t N, int32_t group, void* Y,
-                         int64_t ldy, int32_t* Acc, void* ws, size_t ws_bytes, cudaStream_t st) {
+                         int64_t ldy, int32_t* Acc, void* ws, size_t ws_bytes, cudaStream_t st,
+                         const void* We = nullptr) {
   if (!bits || M < 0 || N < 0 || K <= 0) return COMET_ERR_INVALID_ARG;
   if (K % 128 || N % 128 || K > 65536) return COMET_ERR_SHAPE;
   if (group != 128 && group != K) return COMET_ERR_SHAPE;
@@ -406,8 +416,9 @@ comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, in
   a.splits = p.splits;
   a.ws_counter = reinterpret_cast<int*>(ws);
   a.ws_partial = ws ? reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + kCounterBytes) : nullptr;
-  if (Acc) return launch_gemm<true>(tmW, tmX4, tmX8, map, a, p, st);
-  return launch_gemm<false>(tmW, tmX4, tmX8, map, a, p, st);
+  if (We && !aligned16(We)) return COMET_ERR_ALIGNMENT;
+  if (Acc) return launch_gemm<true>(tmW, tmX4, tmX8, map, a, p, st, We);
+  return launch_gemm<false>(tmW, tmX4, tmX8, map, a, p, st, We);
 }
 
 int64_t plane_bytes(int32_t M, int32_t K, const uint8_t* bits, int want) {
@@ -553,6 +564,28 @@ comet_status comet_w4ax_gemm(const int8_t* Xq8, const void* Xq4, const float* Sx
                              comet_stream_t stream) {
   return gemm_common(Xq8, Xq4, Sx, ldsx, block_bits, M, K, Wq, Sw, N, group, Y, ldy, nullptr, workspace,
                      workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+comet_status comet_w4ax_gemm_ex(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
+                                const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq, const void* We,
+                                const float* Sw, int32_t N, int32_t group, void* Y, int64_t ldy, void* workspace,
+                                size_t workspace_bytes, comet_stream_t stream) {
+  return gemm_common(Xq8, Xq4, Sx, ldsx, block_bits, M, K, Wq, Sw, N, group, Y, ldy, nullptr, workspace,
+                     workspace_bytes, reinterpret_cast<cudaStream_t>(stream), We);
+}
+
+comet_status comet_expand_weight(const void* Wq, int32_t N, int32_t K, void* We, comet_stream_t stream) {
+  if (N < 0 || K <= 0) return COMET_ERR_INVALID_ARG;
+  if (K % 128 || N % 128 || K > 65536) return COMET_ERR_SHAPE;
+  if (N == 0) return COMET_OK;
+  if (!Wq || !We) return COMET_ERR_INVALID_ARG;
+  if (!aligned16(Wq) || !aligned16(We)) return COMET_ERR_ALIGNMENT;
+  comet_status ds = device_check(nullptr);
+  if (ds != COMET_OK) return ds;
+  const int64_t items = (int64_t)N * (K / 32);
+  expand_weights_kernel<<<(unsigned)((items + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const uint8_t*>(Wq), N, K, reinterpret_cast<uint4*>(We));
+  return check_launch();
 }
 
 comet_status comet_w4ax_gemm_acc_i32(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,

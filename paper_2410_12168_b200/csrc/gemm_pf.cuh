@@ -198,11 +198,14 @@ __host__ __device__ constexpr int pf_col(int h, int j) {
                                                      : PfCfg::kRows + PfCfg::kItemN / 2 * h + j - PfCfg::kItemN / 2);
 }
 
-template <bool kGroupK, bool kAccOut>
+// kXW: the weights come pre-expanded (INT8 = 16 x INT4, comet_expand_weight)
+// and are TMA-loaded straight into the B stage; the staging warps then only
+// expand tokens (comet_w4ax_gemm_ex)
+template <bool kGroupK, bool kAccOut, bool kXW = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
     w4ax_gemm_pf_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmX4,
-                        const __grid_constant__ CUtensorMap tmX8, const __grid_constant__ BlockMap map, GemmArgs args,
-                        PfSched sched) {
+                        const __grid_constant__ CUtensorMap tmX8, const __grid_constant__ CUtensorMap tmWE,
+                        const __grid_constant__ BlockMap map, GemmArgs args, PfSched sched) {
   using C = PfCfg;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
@@ -295,7 +298,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
       pf_wait<COMET_PF_SLEEP & 1>(&lempty[l], ((g / C::kLStages) & 1) ^ 1);
       // XPRE: the tokens land in operand stage g % kStages, free once the MMAs
       // of block g - kStages are done
-      if (C::kXPre && !wrole) pf_wait<COMET_PF_SLEEP & 1>(&mdone[g % C::kStages], ((g / C::kStages) & 1) ^ 1);
+      if ((C::kXPre && !wrole) || (kXW && wrole))
+        pf_wait<COMET_PF_SLEEP & 1>(&mdone[g % C::kStages], ((g / C::kStages) & 1) ^ 1);
       if (elect_one()) trace(tr_cta, wrole ? 14 : 15, g);
       if (!kAccOut && !wrole) pf_wait<COMET_PF_SLEEP & 1>(&sempty[a], ((g / C::kScaleSlots) & 1) ^ 1);
       const uint32_t code = map.code[b];
@@ -303,7 +307,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
       const int rank = code & 0x7FFF;
       const int my_m0 = pm0 + 128 * (int)crank;
       if (elect_one()) {
-        if (wrole) {
+        if (wrole && kXW) {
+          // pre-expanded weights: one SW128 box of the CTA's kRows rows x 128 B
+          // straight into operand stage g % kStages (rows past N zero-filled)
+          const int R = pn0 + C::kRows * (int)crank;
+          mbar_arrive_expect_tx(&lfull[l], C::kRows * 128);
+          tma_load_2d(smem + (g % C::kStages) * C::kWEBytes, &tmWE, &lfull[l], b * 128, R);
+        } else if (wrole) {
           // this CTA's weight rows [R, R + v) of the tile (v < 96 at the right
           // edge of N); in the tiled layout they are contiguous within each
           // 128-row slab
@@ -396,7 +406,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
   } else if (warp >= C::kStageWarp && warp < C::kStageWarp + 4) {
     // ---- a4 staging (thread = token row of lane quarter q) ----
     // (XPRE: the tokens arrive expanded in smem; only the weights are staged)
-    constexpr bool do_tok = !C::kXPre, do_w = true;
+    constexpr bool do_tok = !C::kXPre, do_w = !kXW;
     const int q = warp & 3;
     const int et = (int)threadIdx.x - 32 * C::kStageWarp;  // weight-expanding thread 0..127
     const uint32_t tst = tmem_base + ((uint32_t)(32 * q) << 16) + C::kAOff;
@@ -744,6 +754,26 @@ __global__ void __launch_bounds__(256) expand_int4_tokens_kernel(const uint4* __
     out[2 * i] = o0;
     out[2 * i + 1] = o1;
   }
+}
+
+// comet_expand_weight: tiled packed weights -> row-major INT8 We [N x K],
+// We[n, k] = 16 * wq[n, k] (the zero-extension of P:L294 done once, offline;
+// the nibble order makes lo/hi of each word elements 0-3 / 4-7)
+__global__ void __launch_bounds__(256) expand_weights_kernel(const uint8_t* __restrict__ Wq, int N, int K,
+                                                             uint4* __restrict__ out) {
+  const int nb = K / 128, cpr = K / 32;  // 16-B packed chunks per row
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)N * cpr) return;
+  const int64_t n = i / cpr;
+  const int c = (int)(i % cpr);
+  const uint4 w = *reinterpret_cast<const uint4*>(Wq + wq_tiled_offset(n, (int64_t)c * 16, nb));
+  uint4 o0, o1;
+  zext_word(w.x, o0.x, o0.y);
+  zext_word(w.y, o0.z, o0.w);
+  zext_word(w.z, o1.x, o1.y);
+  zext_word(w.w, o1.z, o1.w);
+  out[2 * i] = o0;
+  out[2 * i + 1] = o1;
 }
 
 }  // namespace comet
