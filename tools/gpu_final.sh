@@ -28,3 +28,5 @@ if [ "$1" == "ncu" ]; then
 fi
 
 bash tools/profile_round.sh
+run 7b_xw --steps 20 --warmup 5 --no-cpu-baseline --expanded-weights
+run 70b_xw --config llama3-70b --steps 10 --warmup 3 --no-cpu-baseline --expanded-weights
