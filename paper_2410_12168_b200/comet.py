@@ -324,6 +324,10 @@ def comet_w4ax_gemm_ex(Xq8, Xq4, Sx, bits, Wq, We, Sw, group: int = BLOCK, out: 
     b = as_bits(bits)
     M = Xq8.shape[0] if b.n8 else Xq4.shape[0]
     N, K = Wq.shape[0], Wq.shape[1] * 2
+    if We is not None:
+        # the library builds We's TMA map as [N x K] int8 from Wq's shape: anything else would be read out of bounds
+        if not (We.is_cuda and We.dtype == torch.int8 and tuple(We.shape) == (N, K) and We.stride() == (K, 1)):
+            raise CometError("comet_w4ax_gemm_ex", 1)
     Y = out if out is not None else torch.empty((M, N), dtype=torch.float16, device=Wq.device)
     need = comet_w4ax_gemm_workspace_bytes(M, N, K)
     if need > 0 and (workspace is None or workspace.numel() < need):

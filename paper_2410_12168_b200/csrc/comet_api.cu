@@ -142,6 +142,23 @@ bool make_map_f16(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows
   return r == CUDA_SUCCESS;
 }
 
+// ---- per-device opt-in to large dynamic shared memory -----------------------
+// cudaFuncSetAttribute applies to the current device only: remember, per
+// kernel and per device, that it succeeded (a failure is not cached)
+struct AttrCache {
+  std::atomic<uint64_t> done{0};
+  cudaError_t set(const void* kern, int smem) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+  }
+};
+
 // ---- block map ------------------------------------------------------------
 bool build_block_map(const uint8_t* bits, int nb, BlockMap* map, int* n8, int* n4) {
   int r8 = 0, r4 = 0;
@@ -199,9 +216,8 @@ comet_status launch_gemm_2sm(const CUtensorMap& tmW, const CUtensorMap& tmX4, co
                              const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
   using C = Gemm2Cfg;
   auto kern = w4ax_gemm_2sm_kernel<kGroupK, kAcc>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes); });
+  static AttrCache cache;
+  cudaError_t attr_err = cache.set(reinterpret_cast<const void*>(kern), C::kSmemBytes);
   if (attr_err != cudaSuccess) return cuda_fail(attr_err);
   // a8: Y [M x N] fp16 (row stride ldy), stored in 32-row x 64-column boxes
   CUtensorMap tmY = tmX4;  // never dereferenced on the INT32 debug path
@@ -223,9 +239,8 @@ comet_status launch_gemm_pf(const CUtensorMap& tmX4, const CUtensorMap& tmX8, co
                             const GemmArgs& args, const Plan& p, cudaStream_t st, const void* We = nullptr) {
   using C = PfCfg;
   auto kern = w4ax_gemm_pf_kernel<kGroupK, kAcc, kXW>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes); });
+  static AttrCache cache;
+  cudaError_t attr_err = cache.set(reinterpret_cast<const void*>(kern), C::kSmemBytes);
   if (attr_err != cudaSuccess) return cuda_fail(attr_err);
   // a8: Y [M x N] fp16 (row stride ldy), stored in 32-row x 16-column boxes
   CUtensorMap tmY = tmX4;  // never dereferenced on the INT32 debug path
@@ -257,9 +272,8 @@ comet_status launch_decode(const DecMaps& dm, const CUtensorMap& tmX4, const CUt
                            const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
   using C = DecCfg<BN>;
   auto kern = w4ax_gemm_decode_kernel<BN, kGroupK, kAcc>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes); });
+  static AttrCache cache;
+  cudaError_t attr_err = cache.set(reinterpret_cast<const void*>(kern), C::kSmemBytes);
   if (attr_err != cudaSuccess) return cuda_fail(attr_err);
   DecSched sched;
   sched.n_tiles = p.n_tiles;
@@ -510,7 +524,10 @@ int64_t comet_w4ax_linear_scratch_bytes(int32_t M, int32_t N, int32_t K, const u
   if (p8 < 0 || p4 < 0 || ws < 0) return -1;
   int64_t sx = (K / 128) * comet_act_ldsx(M) * 4;
   int64_t io = align256((int64_t)M * K * 2) + align256((int64_t)M * N * 2);  // staging for host X / Y
-  return align256(ws > 0 ? ws : 0) + align256(p8) + align256(p4) + align256(sx) + align256(io) + 256;
+  // the GEMM workspace sits at the scratch base and is never shorter than the
+  // stream-K tile counters, so a prefill call (no workspace) never overwrites
+  // the counters a later decode call on the same scratch relies on
+  return align256(std::max<int64_t>(ws, kCounterBytes)) + align256(p8) + align256(p4) + align256(sx) + align256(io) + 256;
 }
 
 comet_status comet_pack_weight(const void* W, int64_t ldw, int32_t N, int32_t K, const int32_t* perm, int32_t group,
@@ -606,6 +623,12 @@ comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K,
   if (M == 0 || N == 0) return COMET_OK;
   if (!X || !Y || !Wq || !Sw) return COMET_ERR_INVALID_ARG;
   if (!scratch || (int64_t)scratch_bytes < need) return COMET_ERR_WORKSPACE;
+  // everything comet_quantize_act / comet_w4ax_gemm would reject is checked
+  // before the first copy or launch, so a failed call has no side effects
+  if (group != 128 && group != K) return COMET_ERR_SHAPE;
+  if (K > 65536) return COMET_ERR_SHAPE;
+  if (!aligned16(Wq) || !aligned16(Sw) || (perm && !aligned16(perm)) || !aligned16(scratch)) return COMET_ERR_ALIGNMENT;
+  if (make_plan(M, N, K, 148).ws_bytes < 0) return COMET_ERR_SHAPE;
   comet_status ds = device_check(nullptr);
   if (ds != COMET_OK) return ds;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -619,8 +642,8 @@ comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K,
 
   char* p = reinterpret_cast<char*>(scratch);
   const int64_t ws_bytes = comet_w4ax_gemm_workspace_bytes(M, N, K);
-  void* ws = ws_bytes > 0 ? p : nullptr;  // counters must stay at the scratch base (zeroed once)
-  p += align256(ws_bytes > 0 ? ws_bytes : 0);
+  void* ws = ws_bytes > 0 ? p : nullptr;  // counters stay at the scratch base (zeroed once, reset by the kernel)
+  p += align256(std::max<int64_t>(ws_bytes, kCounterBytes));
   const int64_t p8 = plane_bytes(M, K, block_bits, 8), p4 = plane_bytes(M, K, block_bits, 4);
   int8_t* Xq8 = reinterpret_cast<int8_t*>(p);
   p += align256(p8);

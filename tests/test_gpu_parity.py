@@ -257,3 +257,87 @@ def test_linear_entry_with_host_buffers():
     scratch = comet.new_workspace(comet.comet_w4ax_linear_scratch_bytes(100, 512, 1024, bits), W.device)
     comet.comet_w4ax_linear(Xh, bits, Wq, Sw, perm=perm, out=Yh, scratch=scratch)
     assert np.array_equal(Yh.numpy().view(np.uint16), g["Y"].view(np.uint16))
+
+
+def test_linear_prefill_then_decode_same_scratch():
+    """a prefill call (no GEMM workspace) must not overwrite the
+    stream-K tile counters a later decode call on the same scratch uses."""
+    bits_np = synth.block_bits_for(4096, 3)
+    bits = comet.BlockBits(bits_np)
+    pre = synth.make_problem(4096, 4096, 4096, n8=3, seed=21)
+    dec = synth.make_problem(16, 4096, 4096, n8=3, seed=22)
+    dec["perm"], dec["W"] = pre["perm"], pre["W"]  # one layer, two calls
+    W, perm = to_dev(pre["W"]), to_dev(pre["perm"])
+    Wq, Sw = comet.comet_pack_weight(W, perm, 128)
+    need = max(comet.comet_w4ax_linear_scratch_bytes(m, 4096, 4096, bits) for m in (4096, 16))
+    scratch = torch.full((need,), 0, dtype=torch.uint8, device=W.device)
+    for p in (pre, dec, dec):
+        X = to_dev(p["X"])
+        Y = comet.comet_w4ax_linear(X, bits, Wq, Sw, perm=perm, scratch=scratch)
+        torch.cuda.synchronize()
+        ref = gpu_path(p, 128)["Y"]
+        assert np.array_equal(Y.cpu().numpy().view(np.uint16), ref.view(np.uint16))
+
+
+def acc_sampled(p, group, rows):
+    """GPU per-block INT32 accumulators of the full problem, sampled rows."""
+    X, W, perm = to_dev(p["X"]), to_dev(p["W"]), to_dev(p["perm"])
+    bits = comet.BlockBits(p["bits"])
+    Wq, Sw = comet.comet_pack_weight(W, perm, group)
+    Xq8, Xq4, Sx = comet.comet_quantize_act(X, bits, perm)
+    Acc = comet.comet_w4ax_gemm_acc_i32(Xq8, Xq4, Sx, bits, Wq, Sw, group)
+    out = Acc[:, torch.from_numpy(rows).long().cuda(), :].cpu().numpy()
+    del Acc
+    torch.cuda.empty_cache()
+    return out
+
+
+@pytest.mark.parametrize("M,N,K,n8,group", [(4096, 11008, 4096, 3, 128), (2048, 8192, 28672, 22, 128),
+                                             (16, 57344, 8192, 6, 128), (8192, 6144, 4096, 3, 4096)])
+def test_full_size_acc_i32_sampled_rows(M, N, K, n8, group):
+    """INT32 bit-exactness in the launch configurations the bench runs:
+    multi-tile persistent prefill loops (ring phases flip across tiles) and
+    multi-unit stream-K decode; 64 sampled rows (first, last, seeded random)."""
+    p = synth.make_problem(M, N, K, n8=n8, seed=310)
+    rows = synth.sample_rows(M, 64 if M > 64 else M)
+    g = acc_sampled(p, group, rows)
+    Xq8, Xq4, Sx = oracle.quantize_act(p["X"], p["bits"], p["perm"])
+    Wq, Sw = oracle.pack_weight(p["W"], group, p["perm"])
+    r = oracle.w4ax_gemm(Xq8, Xq4, Sx, p["bits"], Wq, Sw, group=group, rows=rows, want_acc=True)
+    assert g.shape == r["acc"].shape
+    assert np.array_equal(g, r["acc"])
+
+
+def pow2_problem(M, N, K, n8, seed):
+    """P11 inputs: every (row, block) absmax is qmax * 2^e (INT4 blocks 7 * 1,
+    INT8 blocks 127 * 0.25) and every weight group's absmax is 7 * 0.5, all
+    values on those lattices: every scale, product and partial sum is exact."""
+    rng = np.random.default_rng(seed)
+    bits = synth.block_bits_for(K, n8, "scattered")
+    X = rng.integers(-7, 8, (M, K)).astype(np.float64)
+    sgn = lambda shape: np.where(rng.integers(0, 2, shape) == 1, 1.0, -1.0)
+    for b in range(K // 128):
+        if bits[b] == 8:
+            X[:, b * 128:(b + 1) * 128] = rng.integers(-127, 128, (M, 128)) * 0.25
+            X[:, b * 128] = 127 * 0.25 * sgn(M)
+        else:
+            X[:, b * 128] = 7 * sgn(M)
+    W = rng.integers(-7, 8, (N, K)).astype(np.float64) * 0.5
+    W[:, 0::128] = 3.5 * sgn((N, K // 128))
+    return {"X": X.astype(np.float16), "W": W.astype(np.float16), "perm": None, "bits": bits}
+
+
+@pytest.mark.parametrize("M,group", [(300, 128), (300, 4096), (4096, 128), (4096, 4096)])
+def test_power_of_two_scales_bit_exact_prefill(M, group):
+    """P11 on the prefill kernel (M > 128) with N = 14336 >= 74 clusters x 192
+    (every cluster runs tiles; M = 4096 loops several tiles per cluster):
+    fp16 Y bit-equal to the oracle on 64 sampled rows."""
+    N, K = 14336, 4096
+    p = pow2_problem(M, N, K, 3, seed=40 + M)
+    g = gpu_path(p, group)
+    rows = synth.sample_rows(M, 64)
+    Xq8, Xq4, Sx = oracle.quantize_act(p["X"], p["bits"], None)
+    Wq, Sw = oracle.pack_weight(p["W"], group, None)
+    r = oracle.w4ax_gemm(Xq8, Xq4, Sx, p["bits"], Wq, Sw, group=group, rows=rows, want_y64=True)
+    assert np.array_equal(r["y64"], p["X"][rows].astype(np.float64) @ p["W"].astype(np.float64).T)
+    assert np.array_equal(g["Y"][rows].view(np.uint16), r["y"].view(np.uint16))
