@@ -2,28 +2,38 @@
 """Benchmark of the COMET W4Ax hot path on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl comet|reference] [--config NAME]
+                    [--group 128|channel] [--no-alt-group] [--no-cpu-baseline]
 
-Workload (default, BASELINE.json configs[1]): LLaMA-2-7B linear shapes,
-K=4096, N in {4096, 11008}, M=4096 tokens (the top of the M=1..4096 range),
-3/32 INT8 blocks (~10%), INT4 weights with per-output-channel scales
-(--group 128 for 128-channel groups), seeded synthetic inputs
-(paper_2410_12168_b200.synth).  One step = one pass of the hot path over
-both layers: quantize_act (a1+a2) + w4ax_gemm (a3..a8) per layer
-(+ the NCCL all-gather of Y when N>1: weights N-sharded, X replicated).
+Workload (default): BASELINE.json configs[2], the largest single-GPU
+configuration -- LLaMA-3-8B linear shapes QKV (6144x4096), O (4096x4096),
+gate_up (28672x4096), down (4096x14336) at prefill M=8192 tokens, ~10% INT8
+blocks (3/32, 11/112), INT4 weights with 128-channel group scales (SURVEY
+8(d) C3), seeded synthetic inputs (paper_2410_12168_b200.synth).  One step =
+one pass of the hot path over every layer: comet_quantize_act (a1+a2) +
+comet_w4ax_gemm (a3..a8) per layer; with N > 1 GPUs the weights are N-sharded
+(tensor parallel), X is replicated, and each layer's Y shards are all-gathered
+(NCCL) and reassembled into Y [M x N] by comet_gather_shards inside the step.
 Weights are packed once before timing (a0 is offline); its time is
-reported separately as pack_weight_ms.
+reported as pack_weight_ms.  The same step with the other weight-scale
+granularity (per output channel) is timed too and reported under
+"alt_weight_scales".
 
-Timing: W untimed warm-up steps, then K steps; L2 is flushed (256 MiB
-write) before every timed step outside the timed events; each step is
-timed with CUDA events on the launching stream and summed; barrier +
-synchronize on both sides; max over ranks.  Rank 0 prints ONE JSON line.
+Timing: W >= 3 untimed warm-up steps, then K steps.  At N = 1 a step is one
+replay of a CUDA graph of the step's launches; every step is bracketed by CUDA
+events on the launching stream, L2 is flushed (256 MiB write) before every
+step outside the events; value uses the median step (p10/p90 reported);
+barrier + synchronize around the timed region; max over ranks.  Rank 0 prints
+ONE JSON line.  With --gpus N > 1 and no torchrun environment, bench.py
+re-launches itself under torch.distributed.run with N ranks (127.0.0.1).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -34,23 +44,32 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "W4Ax GEMM TOPS & % of B200 INT8/HBM roofline; linear-layer tokens/s at 1/2/4/8 GPU"
-PREROLL_CYCLES = 1_000_000  # ~0.5 ms GPU spin ahead of each timed step (host launch overhead hidden)
+PREROLL_CYCLES = 1_000_000  # ~0.5 ms GPU spin ahead of each short timed step (host launch gaps hidden)
 
+_8B = [(6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336)]
+_70B = [(10240, 8192), (8192, 8192), (57344, 8192), (8192, 28672)]
 CONFIGS = {
+    # BASELINE.json configs[2]: the largest single-GPU configuration (default)
+    "llama3-8b": dict(workload="LLaMA-3-8B QKV/O/gate_up/down (K=4096/14336), prefill M=8192, 3/32 + 11/112 INT8 blocks",
+                      M=8192, layers=_8B, n8=[3, 3, 3, 11], seed=200),
+    # BASELINE.json configs[3]: LLaMA-3-70B linear shapes (single-GPU share; N-sharded for N > 1)
+    "llama3-70b": dict(workload="LLaMA-3-70B QKV/O/gate_up/down (K=8192/28672), prefill M=8192, 6/64 + 22/224 INT8 blocks",
+                       M=8192, layers=_70B, n8=[6, 6, 6, 22], seed=300),
+    "llama3-70b-16k": dict(workload="LLaMA-3-70B QKV/O/gate_up/down, prefill M=16384, 6/64 + 22/224 INT8 blocks",
+                           M=16384, layers=_70B, n8=[6, 6, 6, 22], seed=300),
+    "llama3-70b-mlp": dict(workload="LLaMA-3-70B gate_up (57344x8192) + down (8192x28672), M=8192, 6/64 + 22/224 INT8",
+                           M=8192, layers=_70B[2:], n8=[6, 22], seed=302),
+    "llama3-70b-decode": dict(workload="LLaMA-3-70B QKV/O/gate_up/down, decode M=16, 6/64 + 22/224 INT8 blocks",
+                              M=16, layers=_70B, n8=[6, 6, 6, 22], seed=300),
     # BASELINE.json configs[1]
     "llama2-7b": dict(workload="LLaMA-2-7B linear shapes (K=4096, N=4096/11008), M=4096, 3/32 INT8 blocks",
-                      M=4096, layers=[(4096, 4096), (11008, 4096)], n8=[3, 3]),
-    # decode point of the same config
+                      M=4096, layers=[(4096, 4096), (11008, 4096)], n8=[3, 3], seed=100),
     "llama2-7b-decode": dict(workload="LLaMA-2-7B linear shapes (K=4096, N=4096/11008), M=16 decode, 3/32 INT8 blocks",
-                             M=16, layers=[(4096, 4096), (11008, 4096)], n8=[3, 3]),
-    # BASELINE.json configs[3] (single-GPU share of the 70B prefill)
-    "llama3-70b": dict(workload="LLaMA-3-70B gate_up (57344x8192) + down (8192x28672), M=8192, 6/64 + 22/224 INT8",
-                       M=8192, layers=[(57344, 8192), (8192, 28672)], n8=[6, 22]),
-    "llama3-70b-decode": dict(workload="LLaMA-3-70B gate_up + down, M=16 decode", M=16,
-                              layers=[(57344, 8192), (8192, 28672)], n8=[6, 22]),
+                             M=16, layers=[(4096, 4096), (11008, 4096)], n8=[3, 3], seed=100),
     # BASELINE.json configs[0]
-    "tiny": dict(workload="tiny W4Ax GEMM M=16 N=256 K=512, one INT8 block", M=16, layers=[(256, 512)], n8=[1]),
+    "tiny": dict(workload="tiny W4Ax GEMM M=16 N=256 K=512, one INT8 block", M=16, layers=[(256, 512)], n8=[1], seed=0),
 }
+DEFAULT_CONFIG = "llama3-8b"
 
 
 def load_peaks():
@@ -60,16 +79,27 @@ def load_peaks():
         return {"hbm_gbs": pk["hbm_gbs"], "bf16_tflops": pk["bf16_tflops"],
                 "bf16_tflops_sustained": pk.get("bf16_tflops_sustained"), "src": "measured"}
     except Exception:
+        # /opt/skills/guides/B200_PROFILING.md fallback figures
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "src": "fallback"}
 
 
-def load_traffic(config_name):
+def load_traffic(config_name, group):
     """dram bytes per GEMM launch from a committed ncu --set full summary."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f).get(config_name)
+            return json.load(f).get(f"{config_name}/g{group}")
     except Exception:
         return None
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 # ------------------------------------------------------------ clocks ----
@@ -121,7 +151,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------ distributed ----
-def dist_setup(ngpus):
+def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1:
         import torch
@@ -133,20 +163,39 @@ def dist_setup(ngpus):
     return 0, 1, 0
 
 
+def relaunch_distributed(ngpus: int) -> int:
+    """--gpus N > 1 without a torchrun environment: run N ranks of this
+    script under torch.distributed.run on 127.0.0.1 (rank 0 prints)."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ngpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def group_of(group, K):
+    """weight-scale group size: 128 or K (per output channel)"""
+    return K if group == "channel" else 128
+
+
+def percentile(v, q):
+    return float(np.percentile(np.asarray(v, dtype=np.float64), q))
+
+
 # ---------------------------------------------------------- reference ----
 def run_reference(args, cfg):
     """--impl reference: the CPU oracle as it stands on the host cores."""
     import oracle
     from paper_2410_12168_b200 import synth
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    if int(os.environ.get("RANK", "0")) != 0:
         return 0
     M = cfg["M"]
-    rows = synth.sample_rows(M, 4 if M > 4 else M, seed=1)
+    rows = synth.sample_rows(M, min(16, M), seed=1)
     layers = []
     for li, ((N, K), n8) in enumerate(zip(cfg["layers"], cfg["n8"])):
-        p = synth.make_problem(M, N, K, n8=n8, seed=100 + li, x_rows=rows)
-        g = group_of(args, K)
+        p = synth.make_problem(M, N, K, n8=n8, seed=cfg["seed"] + li, x_rows=rows)
+        g = group_of(args.group, K)
         Wq, Sw = oracle.pack_weight(p["W"], g, p["perm"])
         layers.append((p, Wq, Sw, g))
 
@@ -164,11 +213,13 @@ def run_reference(args, cfg):
     ops = sum(2.0 * len(rows) * N * K for (N, K) in cfg["layers"])
     tops = ops / dt / 1e12
     cores = oracle.num_threads()
-    sample = f"{len(rows)} of {M} token rows per layer (quantize+GEMM+dequant, pre-packed weights)"
+    sample = (f"{len(rows)} of {M} token rows per layer, every layer of the workload "
+              f"(quantize + per-block INT32 GEMM + fp64 dequant, pre-packed weights); host: {cpu_model()}")
     out = {"impl": "reference", "metric": METRIC, "value": tops, "unit": "TOPS", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-           "scaling": "strong", "vs_baseline": None, "dtype": "int8/int32+f64", "data": "synthetic",
-           "config": {"workload": cfg["workload"], "M": M, "layers": cfg["layers"], "weight_scales": args.group},
+           "scaling": "weak", "vs_baseline": None, "dtype": "int8/int32 + f64 dequant", "data": "synthetic",
+           "config": {"workload": cfg["workload"], "M": M, "layers": cfg["layers"],
+                      "weight_scales": args.group if args.group == "channel" else "group128"},
            "tokens_per_s": len(rows) / dt,
            "cpu_baseline": {"value": tops, "unit": "TOPS", "cores": cores, "kind": "oracle", "sample": sample},
            "e2e": {"value": tops, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -176,22 +227,16 @@ def run_reference(args, cfg):
     return 0
 
 
-def group_of(args, K):
-    """weight-scale group size: K (per output channel) or 128"""
-    return K if args.group == "channel" else 128
-
-
 def cpu_baseline(cfg, args, seconds_target=10.0):
     """Oracle timed on the host cores on a bounded row sample (rank 0, N=1)."""
     import oracle
     from paper_2410_12168_b200 import synth
     M = cfg["M"]
-    nrows = 8 if M >= 8 else M
-    rows = synth.sample_rows(M, nrows, seed=2)
+    rows = synth.sample_rows(M, min(64, M), seed=2)
     layers = []
     for li, ((N, K), n8) in enumerate(zip(cfg["layers"], cfg["n8"])):
-        p = synth.make_problem(M, N, K, n8=n8, seed=100 + li, x_rows=rows)
-        g = group_of(args, K)
+        p = synth.make_problem(M, N, K, n8=n8, seed=cfg["seed"] + li, x_rows=rows)
+        g = group_of(args.group, K)
         Wq, Sw = oracle.pack_weight(p["W"], g, p["perm"])
         layers.append((p, Wq, Sw, g))
     t0 = time.perf_counter()
@@ -206,8 +251,8 @@ def cpu_baseline(cfg, args, seconds_target=10.0):
     dt = (time.perf_counter() - t0) / reps
     ops = sum(2.0 * len(rows) * N * K for (N, K) in cfg["layers"])
     return {"value": ops / dt / 1e12, "unit": "TOPS", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{len(rows)} of {M} token rows x {len(layers)} layers, {reps} reps "
-                      f"(quantize + per-block INT32 GEMM + fp64 dequant; weights pre-packed)",
+            "sample": f"{len(rows)} of {M} token rows (first, last, seeded random) x {len(layers)} layers, {reps} reps "
+                      f"(quantize + per-block INT32 GEMM + fp64 dequant; weights pre-packed); host: {cpu_model()}",
             "tokens_per_s": len(rows) / dt}
 
 
@@ -217,39 +262,42 @@ def run_comet(args, cfg, config_name):
     import torch.distributed as dist
     from paper_2410_12168_b200 import comet, synth, tp
 
-    rank, world, local = dist_setup(args.gpus)
+    rank, world, local = dist_setup()
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     M = cfg["M"]
-    stream = torch.cuda.current_stream()
+    groups = [args.group] + ([] if args.no_alt_group else [("channel" if args.group == "128" else "128")])
 
     layers = []
     t_pack = 0.0
     for li, ((N, K), n8) in enumerate(zip(cfg["layers"], cfg["n8"])):
-        p = synth.make_problem(M, N, K, n8=n8, seed=100 + li)
+        p = synth.make_problem(M, N, K, n8=n8, seed=cfg["seed"] + li)
         n0, n1, per = tp.shard_rows(N, world, rank)
         W = torch.from_numpy(tp.shard_weight(p["W"], world, rank)).to(dev)
         perm = torch.from_numpy(p["perm"]).to(dev)
         bits = comet.BlockBits(p["bits"])
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        grp = group_of(args, K)
-        e0.record()
-        Wq, Sw = comet.comet_pack_weight(W, perm, grp)
-        e1.record()
-        torch.cuda.synchronize()
-        t_pack += e0.elapsed_time(e1)
+        packed = {}
+        for gname in groups:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            packed[gname] = comet.comet_pack_weight(W, perm, group_of(gname, K))
+            e1.record()
+            torch.cuda.synchronize()
+            if gname == args.group:
+                t_pack += e0.elapsed_time(e1)
+        del W
         X = torch.from_numpy(p["X"]).to(dev)
-        planes = comet.alloc_act_planes(M, K, bits, dev)
-        Y = torch.empty((M, per), dtype=torch.float16, device=dev)
-        ws = comet.new_workspace(comet.comet_w4ax_gemm_workspace_bytes(M, per, K), dev)
-        Yall = torch.empty((world, M, per), dtype=torch.float16, device=dev) if world > 1 else None
-        Xh = torch.from_numpy(p["X"]).pin_memory()
-        Yh = torch.empty((M, per), dtype=torch.float16).pin_memory()
-        scratch = comet.new_workspace(comet.comet_w4ax_linear_scratch_bytes(M, per, K, bits), dev)
-        # --expanded-weights: the prefill kernel reads an offline INT8 copy (a4 done once)
-        We = comet.comet_expand_weight(Wq) if args.expanded_weights else None
-        layers.append(dict(N=N, K=K, grp=grp, per=per, W=W, perm=perm, bits=bits, Wq=Wq, We=We, Sw=Sw, X=X,
-                           planes=planes, Y=Y, ws=ws, Yall=Yall, Xh=Xh, Yh=Yh, scratch=scratch, ev=[], qev=[]))
+        L = dict(N=N, K=K, per=per, perm=perm, bits=bits, packed=packed, X=X,
+                 planes=comet.alloc_act_planes(M, K, bits, dev),
+                 Y=torch.empty((M, per), dtype=torch.float16, device=dev),
+                 ws=comet.new_workspace(comet.comet_w4ax_gemm_workspace_bytes(M, per, K), dev),
+                 Yall=torch.empty((world, M, per), dtype=torch.float16, device=dev) if world > 1 else None,
+                 Yfull=torch.empty((M, N), dtype=torch.float16, device=dev) if world > 1 else None,
+                 Xh=torch.from_numpy(p["X"]).pin_memory(),
+                 Yh=torch.empty((M, per), dtype=torch.float16).pin_memory(),
+                 scratch=comet.new_workspace(comet.comet_w4ax_linear_scratch_bytes(M, per, K, bits), dev),
+                 ev=[], qev=[])
+        layers.append(L)
         del p
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
@@ -260,170 +308,198 @@ def run_comet(args, cfg, config_name):
             L["cplanes"] = {b: comet.alloc_act_planes(b[1] - b[0], L["K"], L["bits"], dev)
                             for b in tp.chunk_bounds(M, chunks)}
 
-            def gemm_rows(m0, m1, out, L=L):
-                Xq8, Xq4, Sx = comet.comet_quantize_act(L["X"][m0:m1], L["bits"], L["perm"], out=L["cplanes"][(m0, m1)])
-                comet.comet_w4ax_gemm_ex(Xq8, Xq4, Sx, L["bits"], L["Wq"], L["We"], L["Sw"], L["grp"], out=out,
-                                         workspace=L["ws"])
-            L["gemm_rows"] = gemm_rows
-
-    def step(timed_kernels=False):
+    def layer_fwd(L, gname, timed=False):
+        Wq, Sw = L["packed"][gname]
+        grp = group_of(gname, L["K"])
         if world > 1 and chunks > 1:
-            for L in layers:
-                if timed_kernels:  # the layer's quantize + GEMM + all-gather pipeline (no per-kernel split)
-                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    a.record(stream)
-                tp.pipelined_linear_allgather(L["gemm_rows"], M, L["per"], chunks, torch.float16, dev)
-                if timed_kernels:
-                    b.record(stream)
-                    L["ev"].append((a, b))
-                    L["qev"].append((a, a))
+            def gemm_rows(m0, m1, out):
+                Xq8, Xq4, Sx = comet.comet_quantize_act(L["X"][m0:m1], L["bits"], L["perm"], out=L["cplanes"][(m0, m1)])
+                comet.comet_w4ax_gemm(Xq8, Xq4, Sx, L["bits"], Wq, Sw, grp, out=out, workspace=L["ws"])
+            y_chunks, bounds = tp.pipelined_linear_allgather(gemm_rows, M, L["per"], chunks, torch.float16, dev)
+            for yc, (m0, m1) in zip(y_chunks, bounds):
+                comet.comet_gather_shards(yc, L["N"], out=L["Yfull"][m0:m1])
             return
+        if timed:
+            qa, qb, gb = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            qa.record()
+        Xq8, Xq4, Sx = comet.comet_quantize_act(L["X"], L["bits"], L["perm"], out=L["planes"])
+        if timed:
+            qb.record()
+        comet.comet_w4ax_gemm(Xq8, Xq4, Sx, L["bits"], Wq, Sw, grp, out=L["Y"], workspace=L["ws"])
+        if timed:
+            gb.record()
+            L["qev"].append((qa, qb))
+            L["ev"].append((qb, gb))
+        if world > 1:
+            tp.all_gather_y(L["Y"], out=L["Yall"])
+            comet.comet_gather_shards(L["Yall"], L["N"], out=L["Yfull"])
+
+    def step(gname):
         for L in layers:
-            if timed_kernels:
-                qa, qb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                qa.record(stream)
-            Xq8, Xq4, Sx = comet.comet_quantize_act(L["X"], L["bits"], L["perm"], out=L["planes"])
-            if timed_kernels:
-                qb.record(stream)
-                L["qev"].append((qa, qb))
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-            comet.comet_w4ax_gemm_ex(Xq8, Xq4, Sx, L["bits"], L["Wq"], L["We"], L["Sw"], L["grp"], out=L["Y"],
-                                     workspace=L["ws"])
-            if timed_kernels:
-                b.record(stream)
-                L["ev"].append((a, b))
-            if world > 1:
-                tp.all_gather_y(L["Y"], out=L["Yall"])
+            layer_fwd(L, gname)
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(max(args.warmup, 3) if args.warmup >= 3 else 3):
-        step()
-    barrier()
+    use_graph = world == 1
+    preroll = M <= 256 and not use_graph
 
-    # ---- device-timed region ----
-    preroll = M <= 256
-    n_launch0 = comet.launch_count()
-    step_ms = []
-    with ClockSampler(local) as clk:
+    def time_steps(gname, nsteps, nwarm):
+        """per-step device times (ms) of nsteps steps; launches per step."""
+        graph = None
+        n0 = comet.launch_count()
+        if use_graph:
+            step(gname)  # eager warm-up (attribute caches, TMA maps)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                n0 = comet.launch_count()
+                with torch.cuda.graph(graph, stream=s):
+                    step(gname)
+                per_step = comet.launch_count() - n0
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+            run = graph.replay
+        else:
+            step(gname)
+            torch.cuda.synchronize()
+            per_step = comet.launch_count() - n0
+            run = lambda: step(gname)  # noqa: E731
+        for _ in range(max(3, nwarm)):
+            run()
         barrier()
-        for _ in range(args.steps):
-            flush.fill_(1)
-            # short (decode) steps: GPU spin outside the events so the host has
-            # enqueued the whole step before the device reaches it (the events
-            # then time kernels, not Python launch gaps). Long prefill steps
-            # enqueue ahead anyway, and the spin costs them ~2% (measured)
-            if preroll:
-                torch.cuda._sleep(PREROLL_CYCLES)
-            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s0.record(stream)
-            # no events between the kernels of a step: an event record between the
-            # quantizer and the GEMM would disable their programmatic-dependent-
-            # launch overlap (measured: 7B decode step 38.7 vs 45.8 us)
-            step(timed_kernels=False)
-            s1.record(stream)
-            step_ms.append((s0, s1))
-        barrier()
-    launches = comet.launch_count() - n_launch0
-    t_dev = sum(a.elapsed_time(b) for a, b in step_ms) / args.steps  # ms per step
+        evs = []
+        with ClockSampler(local) as clk:
+            barrier()
+            for _ in range(nsteps):
+                flush.fill_(1)
+                if preroll:
+                    torch.cuda._sleep(PREROLL_CYCLES)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                run()
+                b.record()
+                evs.append((a, b))
+            barrier()
+        ms = [a.elapsed_time(b) for a, b in evs]
+        del graph
+        return ms, per_step, clk.summary()
 
-    # ---- per-kernel times: a second pass of K steps with events around every
-    # kernel (these feed gemm_us / quantize_us and the roofline's achieved rate) ----
-    with ClockSampler(local) as clk2:
+    # ---- device-timed region (headline granularity) ----
+    step_ms, launches_per_step, clocks = time_steps(args.group, args.steps, args.warmup)
+    t_med = statistics.median(step_ms)
+    t_p10, t_p90 = percentile(step_ms, 10), percentile(step_ms, 90)
+
+    # ---- per-kernel times: a second pass with events around every kernel
+    # (eager; these feed gemm_us / quantize_us and the roofline's achieved rate) ----
+    kern_steps = min(args.steps, 20)
+    if world == 1:
         barrier()
-        for _ in range(args.steps):
+        for _ in range(kern_steps):
             flush.fill_(1)
-            if preroll:
-                torch.cuda._sleep(PREROLL_CYCLES)
-            step(timed_kernels=True)
+            for L in layers:
+                layer_fwd(L, args.group, timed=True)
         barrier()
-    gemm_ms = [sum(a.elapsed_time(b) for a, b in L["ev"]) / len(L["ev"]) for L in layers]
-    quant_ms = [sum(a.elapsed_time(b) for a, b in L["qev"]) / len(L["qev"]) for L in layers]
-    L0 = layers[0]
+    gemm_ms = [statistics.median(a.elapsed_time(b) for a, b in L["ev"]) if L["ev"] else None for L in layers]
+    quant_ms = [statistics.median(a.elapsed_time(b) for a, b in L["qev"]) if L["qev"] else None for L in layers]
+
+    # ---- the other weight-scale granularity ----
+    alt = None
+    if len(groups) > 1:
+        alt_ms, _, _ = time_steps(groups[1], args.steps, args.warmup)
+        alt = groups[1]
 
     # ---- end-to-end through the C ABI with host buffers ----
     barrier()
     e2e_ms = []
-    for it in range(args.warmup + args.steps):
+    for it in range(min(args.warmup, 3) + min(args.steps, 10)):
         barrier()
         t0 = time.perf_counter()
         for L in layers:
-            comet.comet_w4ax_linear(L["Xh"], L["bits"], L["Wq"], L["Sw"], perm=L["perm"], group=L["grp"], out=L["Yh"],
-                                    scratch=L["scratch"])
+            Wq, Sw = L["packed"][args.group]
+            comet.comet_w4ax_linear(L["Xh"], L["bits"], Wq, Sw, perm=L["perm"], group=group_of(args.group, L["K"]),
+                                    out=L["Yh"], scratch=L["scratch"])
         torch.cuda.synchronize()
-        if it >= args.warmup:
+        if it >= min(args.warmup, 3):
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
     e2e_t = statistics.median(e2e_ms)
 
     if world > 1:
-        t = torch.tensor([t_dev, e2e_t] + gemm_ms, dtype=torch.float64, device=dev)
+        t = torch.tensor([t_med, t_p10, t_p90, e2e_t], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_dev, e2e_t, gemm_ms = float(t[0]), float(t[1]), [float(v) for v in t[2:]]
+        t_med, t_p10, t_p90, e2e_t = (float(v) for v in t)
+        if alt:
+            ta = torch.tensor([statistics.median(alt_ms)], dtype=torch.float64, device=dev)
+            dist.all_reduce(ta, op=dist.ReduceOp.MAX)
+            alt_ms = [float(ta[0])]
 
-    ops = sum(2.0 * M * L["N"] * L["K"] for L in layers)
-    tops = ops / (t_dev * 1e-3) / 1e12
+    ops = sum(2.0 * M * L["N"] * L["K"] for L in layers)  # the whole job: every rank's shard
+    tops = ops / (t_med * 1e-3) / 1e12
     e2e_tops = ops / (e2e_t * 1e-3) / 1e12
     h2d = sum(M * L["K"] * 2 for L in layers)
     d2h = sum(M * L["per"] * 2 for L in layers)
 
-    # roofline of the dominant kernel (the GEMM of the largest layer)
+    # roofline of the dominant kernel (the GEMM with the largest time)
     peaks = load_peaks()
-    dom = int(np.argmax(gemm_ms))
-    Ld = layers[dom]
-    ops_d = 2.0 * M * Ld["per"] * Ld["K"]
-    nb = Ld["K"] // 128
-    n8 = Ld["bits"].n8
-    bytes_d = (Ld["per"] * Ld["K"] / 2 + 4 * Ld["per"] * (Ld["K"] // Ld["grp"]) + M * (128 * n8 + 64 * (nb - n8)) + 4 * M * nb
-               + 2 * M * Ld["per"])
-    int8_peak = 2.0 * peaks["bf16_tflops"]  # dense int8 = 2x bf16 (nominal 4.5 vs 2.25 PF)
-    t_tc = ops_d / (int8_peak * 1e12)
-    t_hbm = bytes_d / (peaks["hbm_gbs"] * 1e9)
-    if t_tc >= t_hbm:
-        achieved = ops_d / (gemm_ms[dom] * 1e-3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TOPS",
-                "peak_src": f"{peaks['src']} bf16 burst x2 (int8 = 2x bf16 dense)"}
-    else:
-        achieved = bytes_d / (gemm_ms[dom] * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "peak_src": f"{peaks['src']} copy bandwidth"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    tr = load_traffic(config_name)
-    roof["traffic"] = tr.get(f"layer{dom}") if isinstance(tr, dict) else None
-    roof["kernel"] = f"w4ax_gemm layer{dom} (N={Ld['per']}, K={Ld['K']}), {gemm_ms[dom] * 1e3:.1f} us/launch"
+    roof = None
+    if world == 1:
+        dom = int(np.argmax(gemm_ms))
+        Ld = layers[dom]
+        grp = group_of(args.group, Ld["K"])
+        ops_d = 2.0 * M * Ld["per"] * Ld["K"]
+        nb, n8 = Ld["K"] // 128, Ld["bits"].n8
+        bytes_d = (Ld["per"] * Ld["K"] / 2 + 4 * Ld["per"] * (Ld["K"] // grp) + M * (128 * n8 + 64 * (nb - n8))
+                   + 4 * M * nb + 2 * M * Ld["per"])
+        int8_peak = 2.0 * peaks["bf16_tflops"]  # dense int8 / fp8 = 2x bf16 (nominal 4.5 vs 2.25 PF)
+        if ops_d / (int8_peak * 1e12) >= bytes_d / (peaks["hbm_gbs"] * 1e9):
+            achieved = ops_d / (gemm_ms[dom] * 1e-3) / 1e12
+            roof = {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TOPS",
+                    "peak_src": f"{peaks['src']} bf16 burst x2 (dense int8 and e4m3 are both 2x bf16)"}
+        else:
+            achieved = bytes_d / (gemm_ms[dom] * 1e-3) / 1e9
+            roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "peak_src": f"{peaks['src']} copy bandwidth"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        tr = load_traffic(config_name, args.group)
+        roof["traffic"] = tr.get(f"layer{dom}") if isinstance(tr, dict) else None
+        roof["kernel"] = (f"comet_w4ax_gemm layer{dom} (N={Ld['per']}, K={Ld['K']}, M={M}): token prep + "
+                          f"w4ax_gemm kernel, {gemm_ms[dom] * 1e3:.1f} us/call (median)")
 
+    wsname = "channel" if args.group == "channel" else "group128"
     out = {"metric": METRIC, "value": tops, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": t_dev, "higher_is_better": True, "scaling": "strong",
-           "vs_baseline": None, "dtype": "int8 (INT4/INT8 operands) x int32 accum, fp32 dequant, fp16 out",
-           "data": "synthetic (seeded; X~N(0,1) + planted outlier channels, W~N(0,1/K))",
-           "config": {"workload": cfg["workload"], "M": M, "layers": cfg["layers"], "weight_scales": args.group,
-                      "weights": "INT4 + offline INT8 copy for prefill" if args.expanded_weights else "INT4 packed",
-                      "parallelism": (f"tp{world} (N-sharded, NCCL all-gather of Y"
+           "warmup": args.warmup, "ms_per_step": t_med, "ms_per_step_p10": t_p10, "ms_per_step_p90": t_p90,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+           "dtype": "int8 (INT4 blocks as exact e4m3 x e4m3, INT8 blocks s8 x s8; exact block sums), fp32 dequant, fp16 out",
+           "data": "synthetic (seeded; X~N(0,1) + planted outlier channels, W~N(0,1/K)); random-init weights",
+           "config": {"workload": cfg["workload"], "M": M, "layers": cfg["layers"], "weight_scales": wsname,
+                      "weights": "INT4 packed",
+                      "parallelism": (f"tp{world} (N-sharded; NCCL all-gather of Y + comet_gather_shards to [M x N]"
                                       + (f", {chunks} row chunks pipelining GEMM and all-gather)" if chunks > 1 else ")")
                                       if world > 1 else "single GPU"),
-                      "l2": "flushed (256 MiB write) before every timed step, outside the events",
-                      "preroll": ("GPU spin before each timed step so launches are queued ahead" if preroll else "none"),
-                      "kernel_times": ("second pass of K steps with CUDA events around every kernel (gemm_us, "
-                                       "quantize_us, roofline.achieved); the timed steps carry events only at "
-                                       "step boundaries so the quantizer->GEMM PDL overlap stays intact")},
-           "tokens_per_s": M / (t_dev * 1e-3),
-           "gemm_us": [g * 1e3 for g in gemm_ms],
-           "gemm_us_scope": ("quantize + GEMM + all-gather pipeline per layer (row-chunked)"
-                             if (world > 1 and chunks > 1) else "GEMM kernel"),
-           "quantize_us": [q * 1e3 for q in quant_ms],
-           "quantize_hbm": {"achieved_gbs": [ (2 * M * L["K"] + M * (128 * L["bits"].n8 + 64 * L["bits"].n4)
-                                               + 4 * M * (L["K"] // 128)) / (q * 1e-3) / 1e9 if q > 0 else None
-                                              for L, q in zip(layers, quant_ms)],
+                      "timing": ("CUDA graph replay per step" if use_graph else "stream launches per step")
+                                + f", median of {args.steps} event-timed steps",
+                      "l2": "flushed (256 MiB write) before every timed step, outside the events"},
+           "tokens_per_s": M / (t_med * 1e-3),
+           "gemm_us": [None if g is None else g * 1e3 for g in gemm_ms],
+           "quantize_us": [None if q is None else q * 1e3 for q in quant_ms],
+           "quantize_hbm": {"achieved_gbs": [(2 * M * L["K"] + M * (128 * L["bits"].n8 + 64 * L["bits"].n4)
+                                              + 4 * M * (L["K"] // 128)) / (q * 1e-3) / 1e9 if q else None
+                                             for L, q in zip(layers, quant_ms)],
                             "peak_gbs": peaks["hbm_gbs"]},
            "pack_weight_ms": t_pack,
            "e2e": {"value": e2e_tops, "unit": "TOPS", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                   "ms_per_step": e2e_t, "api": "comet_w4ax_linear (host pinned X in, host Y out)"},
-           "gpu_launches": launches,
+                   "ms_per_step": e2e_t, "api": "comet_w4ax_linear per layer (pinned host X in, host Y out)"},
+           "gpu_launches": launches_per_step * args.steps,
            "roofline": roof,
-           "clocks": clk.summary()}
+           "clocks": clocks}
+    if alt:
+        t_alt = statistics.median(alt_ms)
+        out["alt_weight_scales"] = {"weight_scales": "channel" if alt == "channel" else "group128",
+                                    "value": ops / (t_alt * 1e-3) / 1e12, "unit": "TOPS", "ms_per_step": t_alt}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, args, seconds_target=args.cpu_seconds)
     if rank == 0:
@@ -437,22 +513,23 @@ def run_comet(args, cfg, config_name):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="comet", choices=["comet", "reference"])
-    ap.add_argument("--config", default="llama2-7b", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--group", default="channel", choices=["channel", "128"],
-                    help="weight-scale granularity: per output channel (OmniQuant W4A4 style, default) or 128-groups")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--expanded-weights", action="store_true",
-                    help="prefill GEMM reads an offline INT8 copy of the weights (comet_expand_weight): 2x weight memory")
+    ap.add_argument("--group", default="128", choices=["128", "channel"],
+                    help="weight-scale granularity of the headline: 128-channel groups (SURVEY 8(d)) or per output channel")
+    ap.add_argument("--no-alt-group", action="store_true", help="skip timing the other weight-scale granularity")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--overlap-chunks", type=int, default=0,
                     help="N > 1: row chunks pipelining GEMM and all-gather (0: auto = 4 for M >= 1024, 1: serial)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(args.gpus)
     return run_comet(args, cfg, args.config)
 
 

@@ -84,7 +84,10 @@ typedef void* comet_stream_t; /* cudaStream_t */
 int64_t comet_act_plane8_bytes(int32_t M, int32_t K, const uint8_t* block_bits); /* M*K8   */
 int64_t comet_act_plane4_bytes(int32_t M, int32_t K, const uint8_t* block_bits); /* M*K4/2 */
 int64_t comet_act_ldsx(int32_t M);                                               /* roundup(M,4) */
-/* device workspace comet_w4ax_gemm needs for split-K partials + tile counters */
+/* device workspace comet_w4ax_gemm needs: 64 KiB of stream-K tile counters
+ * (decode, M <= 128) followed by the split-K partials (decode) or by the
+ * INT4 token plane re-encoded as e4m3 bytes, M*K bytes at most, and its
+ * per-(block, row) corrections (prefill, M > 128) */
 int64_t comet_w4ax_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K);
 /* device scratch comet_w4ax_linear needs (planes + scales + gemm workspace) */
 int64_t comet_w4ax_linear_scratch_bytes(int32_t M, int32_t N, int32_t K, const uint8_t* block_bits);
@@ -118,7 +121,7 @@ comet_status comet_quantize_act_bf16(const void* X, int64_t ldx, int32_t M, int3
  * with the integer block sums exact (INT32) and the scale applied per block
  * in fp32 ("divide by 16 in the scaling parameter"), rounded once to
  * fp16.  N % 128 == 0.  workspace: device memory of at least
- * comet_w4ax_gemm_workspace_bytes(M, N, K) bytes whose first 64 KiB must be
+ * comet_w4ax_gemm_workspace_bytes(M, N, K) bytes (16-byte aligned) whose first 64 KiB must be
  * zero on the first use (the kernel leaves it zero again); it may be NULL
  * only if that size is 0. */
 comet_status comet_w4ax_gemm(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
@@ -126,31 +129,26 @@ comet_status comet_w4ax_gemm(const int8_t* Xq8, const void* Xq4, const float* Sx
                              int32_t N, int32_t group, void* Y, int64_t ldy, void* workspace,
                              size_t workspace_bytes, comet_stream_t stream);
 
-/* ---- a4 done offline: pre-expanded weights for the prefill kernel --------
- * comet_expand_weight: We int8 [N x K] (DEVICE, row-major, N*K bytes) with
- *   We[n, k] = 16 * wq[n, k] -- the zero-extension of P:L294 applied once
- *   to the packed weights of comet_pack_weight (Wq, tiled layout) instead of
- *   in every prefill GEMM (twice the weight bytes: a memory-for-speed
- *   option for prefill-heavy layers).
- * comet_w4ax_gemm_ex: comet_w4ax_gemm with the expanded copy: for M > 128
- *   the prefill kernel TMA-loads We straight into its weight operand (no
- *   in-kernel weight expansion); for M <= 128 (HBM-bound decode) it reads the
- *   packed Wq.  Wq is always required, We may be NULL (= comet_w4ax_gemm);
- *   results are identical to comet_w4ax_gemm. */
-comet_status comet_expand_weight(const void* Wq, int32_t N, int32_t K, void* We, comet_stream_t stream);
-comet_status comet_w4ax_gemm_ex(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
-                                const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq, const void* We,
-                                const float* Sw, int32_t N, int32_t group, void* Y, int64_t ldy, void* workspace,
-                                size_t workspace_bytes, comet_stream_t stream);
+/* ---- (e) N-sharded tensor parallelism: reassembly of the gathered Y ------
+ * BJ north_star: weights are sharded by output channel (N) over P ranks,
+ * each rank computes Y_r [M x per] (per = N/P rounded up to 128) and an
+ * all-gather (NCCL) leaves Yall = [P x M x per] fp16, rank-major, on every
+ * rank.  This writes Y [M x N] (row stride ldy) with
+ * Y[m, r*per + j] = Yall[r, m, j] for r*per + j < N.  per % 128 == 0,
+ * N % 128 == 0, P*per >= N, ldy >= N, ldy % 8 == 0; Yall and Y 16-byte
+ * aligned and not overlapping. */
+comet_status comet_gather_shards(const void* Yall, int32_t P, int32_t M, int32_t per, int32_t N, void* Y,
+                                 int64_t ldy, comet_stream_t stream);
 
 /* ---- test/debug: per-block INT32 accumulators ---------------------------
  * Acc int32 [K/128 x M x N]: Acc[(b*M + m)*N + n] = sum_{i in block b}
- * xq[m,i]*wq[n,i] in LOGICAL units (the x16 / x256 zero-extension factors
- * removed), computed by the same tcgen05 pipeline as comet_w4ax_gemm. */
+ * xq[m,i]*wq[n,i] in LOGICAL units (the x16 zero-extension factor and, in
+ * the prefill kernel, the e4m3 offset term removed), computed by the same
+ * tcgen05 pipeline as comet_w4ax_gemm; workspace as for comet_w4ax_gemm. */
 comet_status comet_w4ax_gemm_acc_i32(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
                                      const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq,
-                                     const float* Sw, int32_t N, int32_t group, int32_t* Acc,
-                                     comet_stream_t stream);
+                                     const float* Sw, int32_t N, int32_t group, int32_t* Acc, void* workspace,
+                                     size_t workspace_bytes, comet_stream_t stream);
 
 /* ---- the whole linear layer (user call): quantize_act + w4ax_gemm ------
  * X and Y may be HOST (pinned or pageable) or DEVICE pointers; host buffers

@@ -25,7 +25,7 @@ EXPORTS = ["comet_act_plane8_bytes", "comet_act_plane4_bytes", "comet_act_ldsx",
            "comet_w4ax_linear_scratch_bytes", "comet_pack_weight", "comet_quantize_act", "comet_w4ax_gemm",
            "comet_w4ax_gemm_acc_i32", "comet_w4ax_linear", "comet_calib_absmax", "comet_fmpq_map",
            "comet_quantize_kv", "comet_dequantize_kv", "comet_static_act_scales", "comet_quantize_act_static",
-           "comet_quantize_act_bf16", "comet_expand_weight", "comet_w4ax_gemm_ex",
+           "comet_quantize_act_bf16", "comet_gather_shards",
            "comet_status_str", "comet_last_cuda_error",
            "comet_launch_count"]
 
@@ -67,7 +67,7 @@ def lib():
         L.comet_quantize_act.restype = ctypes.c_int
         L.comet_w4ax_gemm.argtypes = [P, P, P, i64, P, i32, i32, P, P, i32, i32, P, i64, P, sz, P]
         L.comet_w4ax_gemm.restype = ctypes.c_int
-        L.comet_w4ax_gemm_acc_i32.argtypes = [P, P, P, i64, P, i32, i32, P, P, i32, i32, P, P]
+        L.comet_w4ax_gemm_acc_i32.argtypes = [P, P, P, i64, P, i32, i32, P, P, i32, i32, P, P, sz, P]
         L.comet_w4ax_gemm_acc_i32.restype = ctypes.c_int
         L.comet_w4ax_linear.argtypes = [P, i64, i32, i32, P, P, P, P, i32, i32, P, i64, P, sz, P]
         L.comet_w4ax_linear.restype = ctypes.c_int
@@ -79,10 +79,8 @@ def lib():
         L.comet_quantize_kv.restype = ctypes.c_int
         L.comet_dequantize_kv.argtypes = [P, P, P, i32, i32, i32, P, i64, P]
         L.comet_dequantize_kv.restype = ctypes.c_int
-        L.comet_expand_weight.argtypes = [P, i32, i32, P, P]
-        L.comet_expand_weight.restype = ctypes.c_int
-        L.comet_w4ax_gemm_ex.argtypes = [P, P, P, i64, P, i32, i32, P, P, P, i32, i32, P, i64, P, sz, P]
-        L.comet_w4ax_gemm_ex.restype = ctypes.c_int
+        L.comet_gather_shards.argtypes = [P, i32, i32, i32, i32, P, i64, P]
+        L.comet_gather_shards.restype = ctypes.c_int
         L.comet_quantize_act_bf16.argtypes = [P, i64, i32, i32, P, P, P, P, P, i64, P]
         L.comet_quantize_act_bf16.restype = ctypes.c_int
         L.comet_static_act_scales.argtypes = [P, i32, P, P, P, P]
@@ -309,44 +307,28 @@ def comet_w4ax_gemm(Xq8, Xq4, Sx, bits, Wq, Sw, group: int = BLOCK, out: Optiona
     return Y
 
 
-def comet_expand_weight(Wq: torch.Tensor, stream=None) -> torch.Tensor:
-    """Offline a4: packed (tiled) Wq [N x K/2] -> We int8 [N x K] = 16 * wq."""
-    N, K = Wq.shape[0], Wq.shape[1] * 2
-    We = torch.empty((N, K), dtype=torch.int8, device=Wq.device)
-    st = lib().comet_expand_weight(_ptr(Wq), N, K, _ptr(We), _stream(stream))
-    _check("comet_expand_weight", st)
-    return We
-
-
-def comet_w4ax_gemm_ex(Xq8, Xq4, Sx, bits, Wq, We, Sw, group: int = BLOCK, out: Optional[torch.Tensor] = None,
-                       workspace: Optional[torch.Tensor] = None, stream=None):
-    """comet_w4ax_gemm with the pre-expanded weights We (used by the prefill kernel)."""
-    b = as_bits(bits)
-    M = Xq8.shape[0] if b.n8 else Xq4.shape[0]
-    N, K = Wq.shape[0], Wq.shape[1] * 2
-    if We is not None:
-        # the library builds We's TMA map as [N x K] int8 from Wq's shape: anything else would be read out of bounds
-        if not (We.is_cuda and We.dtype == torch.int8 and tuple(We.shape) == (N, K) and We.stride() == (K, 1)):
-            raise CometError("comet_w4ax_gemm_ex", 1)
-    Y = out if out is not None else torch.empty((M, N), dtype=torch.float16, device=Wq.device)
-    need = comet_w4ax_gemm_workspace_bytes(M, N, K)
-    if need > 0 and (workspace is None or workspace.numel() < need):
-        raise CometError("comet_w4ax_gemm_ex", 4)
-    st = lib().comet_w4ax_gemm_ex(_ptr(Xq8) if b.n8 else None, _ptr(Xq4) if b.n4 else None, _ptr(Sx), Sx.shape[1],
-                                  b.ptr, M, K, _ptr(Wq), _ptr(We), _ptr(Sw), N, group, _ptr(Y), Y.stride(0),
-                                  _ptr(workspace), 0 if workspace is None else workspace.numel(), _stream(stream))
-    _check("comet_w4ax_gemm_ex", st)
+def comet_gather_shards(Yall: torch.Tensor, N: int, out: Optional[torch.Tensor] = None, stream=None):
+    """(e): rank-major gathered shards [P x M x per] -> Y [M x N] (padding dropped)."""
+    P, M, per = Yall.shape
+    Y = out if out is not None else torch.empty((M, N), dtype=Yall.dtype, device=Yall.device)
+    st = lib().comet_gather_shards(_ptr(Yall), P, M, per, N, _ptr(Y), Y.stride(0), _stream(stream))
+    _check("comet_gather_shards", st)
     return Y
 
 
-def comet_w4ax_gemm_acc_i32(Xq8, Xq4, Sx, bits, Wq, Sw, group: int = BLOCK, stream=None):
+def comet_w4ax_gemm_acc_i32(Xq8, Xq4, Sx, bits, Wq, Sw, group: int = BLOCK, workspace: Optional[torch.Tensor] = None,
+                            stream=None):
     """Debug: per-block INT32 accumulators [K/128 x M x N] (logical units)."""
     b = as_bits(bits)
     M = Xq8.shape[0] if b.n8 else Xq4.shape[0]
     N, K = Wq.shape[0], Wq.shape[1] * 2
     Acc = torch.empty((K // BLOCK, M, N), dtype=torch.int32, device=Wq.device)
+    need = comet_w4ax_gemm_workspace_bytes(M, N, K)
+    if need > 0 and (workspace is None or workspace.numel() < need):
+        workspace = new_workspace(need, Wq.device)
     st = lib().comet_w4ax_gemm_acc_i32(_ptr(Xq8) if b.n8 else None, _ptr(Xq4) if b.n4 else None, _ptr(Sx), Sx.shape[1],
-                                       b.ptr, M, K, _ptr(Wq), _ptr(Sw), N, group, _ptr(Acc), _stream(stream))
+                                       b.ptr, M, K, _ptr(Wq), _ptr(Sw), N, group, _ptr(Acc), _ptr(workspace),
+                                       0 if workspace is None else workspace.numel(), _stream(stream))
     _check("comet_w4ax_gemm_acc_i32", st)
     return Acc
 

@@ -13,11 +13,11 @@
 
 #include "../../include/comet.h"
 #include "gemm.cuh"
-#include "gemm_2sm.cuh"
 #include "gemm_pf.cuh"
 #include "fmpq_aux.cuh"
 #include "gemm_decode.cuh"
 #include "quantize.cuh"
+#include "tp.cuh"
 
 using namespace comet;
 
@@ -28,6 +28,11 @@ std::atomic<int64_t> g_launches{0};
 
 comet_status cuda_fail(cudaError_t e) {
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+  return COMET_ERR_CUDA;
+}
+// a TMA descriptor the driver refused (bad address, stride or box)
+comet_status map_fail(const char* what) {
+  snprintf(g_cuda_err, sizeof(g_cuda_err), "cuTensorMapEncodeTiled failed for %s", what);
   return COMET_ERR_CUDA;
 }
 // launch with the programmatic-stream-serialization (PDL) attribute: the
@@ -127,21 +132,6 @@ bool make_map_f32(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows
   return r == CUDA_SUCCESS;
 }
 
-// 2-D fp16 tensor [rows x cols] (row stride ld elements), box [box_rows x box_cols]
-bool make_map_f16(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t ld, uint32_t box_cols,
-                  uint32_t box_rows, CUtensorMapSwizzle swz) {
-  EncodeTiledFn enc = get_encode();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {ld * 2};
-  cuuint32_t box[2] = {box_cols, box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
 // ---- per-device opt-in to large dynamic shared memory -----------------------
 // cudaFuncSetAttribute applies to the current device only: remember, per
 // kernel and per device, that it succeeded (a failure is not cached)
@@ -180,11 +170,12 @@ bool build_block_map(const uint8_t* bits, int nb, BlockMap* map, int* n8, int* n
 // ---- GEMM launch plan -----------------------------------------------------
 struct Plan {
   int bn, m_tiles, n_tiles, splits;
-  bool two_sm;   // prefill: CTA-pair kernel (256 tokens x 256 weight rows per pair)
+  bool two_sm;   // prefill: CTA-pair kernel (256 tokens x 192 weight rows per pair)
   int clusters;  // persistent CTA pairs
   int64_t ws_bytes;
 };
 constexpr int64_t kCounterBytes = 64 * 1024;
+int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
 
 Plan make_plan(int M, int N, int K, int num_sms) {
   Plan p;
@@ -193,8 +184,11 @@ Plan make_plan(int M, int N, int K, int num_sms) {
   if (p.two_sm) {
     p.bn = 128;  // token rows per CTA (TMA box height)
     p.m_tiles = (M + 255) / 256;
-    p.n_tiles = (N + 255) / 256;
-    p.ws_bytes = 0;
+    p.n_tiles = (N + PfCfg::kTileN - 1) / PfCfg::kTileN;
+    // workspace: [tile counters (kept for decode calls sharing the buffer)]
+    // [e4m3 token plane, M x K4 bytes (K4 <= K)] [corrections 8 sum(xq), K/128 x ldsx fp32]
+    const int64_t ldsx = ((int64_t)M + 3) / 4 * 4;
+    p.ws_bytes = kCounterBytes + align256((int64_t)M * K) + align256((int64_t)(K / 128) * ldsx * 4);
     p.clusters = num_sms / 2;
     return p;
   }
@@ -212,54 +206,22 @@ Plan make_plan(int M, int N, int K, int num_sms) {
 }
 
 template <bool kGroupK, bool kAcc>
-comet_status launch_gemm_2sm(const CUtensorMap& tmW, const CUtensorMap& tmX4, const CUtensorMap& tmX8,
-                             const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
-  using C = Gemm2Cfg;
-  auto kern = w4ax_gemm_2sm_kernel<kGroupK, kAcc>;
-  static AttrCache cache;
-  cudaError_t attr_err = cache.set(reinterpret_cast<const void*>(kern), C::kSmemBytes);
-  if (attr_err != cudaSuccess) return cuda_fail(attr_err);
-  // a8: Y [M x N] fp16 (row stride ldy), stored in 32-row x 64-column boxes
-  CUtensorMap tmY = tmX4;  // never dereferenced on the INT32 debug path
-  if (!kAcc && !make_map_f16(&tmY, args.Y, (uint64_t)args.N, (uint64_t)args.M, (uint64_t)args.ldy, 64, 32,
-                             CU_TENSOR_MAP_SWIZZLE_128B))
-    return COMET_ERR_CUDA;
-  PairSched sched;
-  sched.m_tiles = p.m_tiles;
-  sched.n_tiles = p.n_tiles;
-  sched.tiles = p.m_tiles * p.n_tiles;
-  sched.clusters = sched.tiles < p.clusters ? sched.tiles : p.clusters;  // persistent: one cluster per SM pair
-  dim3 grid(2 * sched.clusters, 1, 1);
-  kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(tmY, tmX4, tmX8, map, args, sched);
-  return check_launch();
-}
-
-template <bool kGroupK, bool kAcc, bool kXW = false>
-comet_status launch_gemm_pf(const CUtensorMap& tmX4, const CUtensorMap& tmX8, const BlockMap& map,
-                            const GemmArgs& args, const Plan& p, cudaStream_t st, const void* We = nullptr) {
+comet_status launch_gemm_pf(const CUtensorMap& tmXe, const CUtensorMap& tmX8, const BlockMap& map,
+                            const GemmArgs& args, const Plan& p, cudaStream_t st) {
   using C = PfCfg;
-  auto kern = w4ax_gemm_pf_kernel<kGroupK, kAcc, kXW>;
+  auto kern = w4ax_gemm_pf_kernel<kGroupK, kAcc>;
   static AttrCache cache;
   cudaError_t attr_err = cache.set(reinterpret_cast<const void*>(kern), C::kSmemBytes);
   if (attr_err != cudaSuccess) return cuda_fail(attr_err);
-  // a8: Y [M x N] fp16 (row stride ldy), stored in 32-row x 16-column boxes
-  CUtensorMap tmY = tmX4;  // never dereferenced on the INT32 debug path
-  if (!kAcc && !make_map_f16(&tmY, args.Y, (uint64_t)args.N, (uint64_t)args.M, (uint64_t)args.ldy, 16, 32,
-                             CU_TENSOR_MAP_SWIZZLE_NONE))
-    return COMET_ERR_CUDA;
   PfSched sched;
   sched.m_tiles = p.m_tiles;
-  sched.tiles = p.m_tiles * ((args.N + C::kTileN - 1) / C::kTileN);
+  sched.tiles = p.m_tiles * p.n_tiles;
   sched.clusters = sched.tiles < p.clusters ? sched.tiles : p.clusters;
-  dim3 grid(2 * sched.clusters, 1, 1);
-  // plain launch: PDL overlap with the quantizer measured ~1% slower for the
-  // prefill kernel (the decode kernel, whose weight stream can start early,
-  // gains 4-16%); griddepcontrol.wait is a no-op without the attribute
-  CUtensorMap tmWE = tmX4;  // dereferenced only with expanded weights (kXW)
-  if (kXW && !make_map_u8(&tmWE, We, (uint64_t)args.K, (uint64_t)args.N, (uint64_t)args.K, 128, C::kRows,
-                          CU_TENSOR_MAP_SWIZZLE_128B))
-    return COMET_ERR_CUDA;
-  kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(tmY, tmX4, tmX8, tmWE, map, args, sched);
+  // PDL: the prologue (barrier init, TMEM allocation) overlaps the token
+  // preparation kernel; the producers wait for it before their first load
+  cudaError_t e = launch_pdl(kern, dim3(2 * sched.clusters), dim3(C::kThreads), C::kSmemBytes, st, tmXe, tmX8, map,
+                             args, sched);
+  if (e != cudaSuccess) return cuda_fail(e);
   return check_launch();
 }
 
@@ -292,10 +254,10 @@ comet_status launch_decode_maps(const CUtensorMap& tmX4, const CUtensorMap& tmX8
   constexpr int kUB = DecCfg<BN>::kUB;
   DecMaps dm;
   if (!make_map_f32(&dm.sx, args.Sx, (uint64_t)args.ldsx, (uint64_t)args.nb, (uint64_t)args.ldsx, BN, kUB))
-    return COMET_ERR_CUDA;
+    return map_fail("Sx");
   if (!kGroupK && !kAcc) {
     if (!make_map_f32(&dm.sw, args.Sw, (uint64_t)args.N, (uint64_t)args.nb, (uint64_t)args.N, 128, kUB))
-      return COMET_ERR_CUDA;
+      return map_fail("Sw");
   } else {
     dm.sw = dm.sx;  // never dereferenced
   }
@@ -313,41 +275,21 @@ comet_status launch_decode_bn(const CUtensorMap& tmX4, const CUtensorMap& tmX8, 
   }
 }
 
-// prefill kernel selection: the TMEM-A kernel (gemm_pf.cuh) unless
-// COMET_PREFILL=2sm asks for the SMEM-operand CTA-pair kernel (A/B testing)
-bool use_pf() {
-  static const bool pf = [] {
-    const char* e = getenv("COMET_PREFILL");
-    return !(e && strcmp(e, "2sm") == 0);
-  }();
-  return pf;
-}
-
 template <bool kAcc>
-comet_status launch_gemm(const CUtensorMap& tmW, const CUtensorMap& tmX4, const CUtensorMap& tmX8,
-                         const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st,
-                         const void* We = nullptr) {
+comet_status launch_gemm(const CUtensorMap& tmXp, const CUtensorMap& tmX8, const BlockMap& map,
+                         const GemmArgs& args, const Plan& p, cudaStream_t st) {
   const bool group_k = args.group_blocks == args.nb;
-  if (p.two_sm && use_pf() && We) {
-    if (group_k) return launch_gemm_pf<true, kAcc, true>(tmX4, tmX8, map, args, p, st, We);
-    return launch_gemm_pf<false, kAcc, true>(tmX4, tmX8, map, args, p, st, We);
-  }
-  if (p.two_sm && use_pf()) {
-    if (group_k) return launch_gemm_pf<true, kAcc>(tmX4, tmX8, map, args, p, st);
-    return launch_gemm_pf<false, kAcc>(tmX4, tmX8, map, args, p, st);
-  }
   if (p.two_sm) {
-    if (group_k) return launch_gemm_2sm<true, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
-    return launch_gemm_2sm<false, kAcc>(tmW, tmX4, tmX8, map, args, p, st);
+    if (group_k) return launch_gemm_pf<true, kAcc>(tmXp, tmX8, map, args, p, st);
+    return launch_gemm_pf<false, kAcc>(tmXp, tmX8, map, args, p, st);
   }
-  if (group_k) return launch_decode_bn<true, kAcc>(tmX4, tmX8, map, args, p, st);
-  return launch_decode_bn<false, kAcc>(tmX4, tmX8, map, args, p, st);
+  if (group_k) return launch_decode_bn<true, kAcc>(tmXp, tmX8, map, args, p, st);
+  return launch_decode_bn<false, kAcc>(tmXp, tmX8, map, args, p, st);
 }
 
 comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx, const uint8_t* bits,
                          int32_t M, int32_t K, const void* Wq, const float* Sw, int32_t N, int32_t group, void* Y,
-                         int64_t ldy, int32_t* Acc, void* ws, size_t ws_bytes, cudaStream_t st,
-                         const void* We = nullptr) {
+                         int64_t ldy, int32_t* Acc, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (!bits || M < 0 || N < 0 || K <= 0) return COMET_ERR_INVALID_ARG;
   if (K % 128 || N % 128 || K > 65536) return COMET_ERR_SHAPE;
   if (group != 128 && group != K) return COMET_ERR_SHAPE;
@@ -362,58 +304,37 @@ comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, in
   if (Acc == nullptr && ((reinterpret_cast<uintptr_t>(Y) & 15) || (reinterpret_cast<uintptr_t>(Sw) & 15)))
     return COMET_ERR_ALIGNMENT;
   if ((n8 && !Xq8) || (n4 && !Xq4)) return COMET_ERR_INVALID_ARG;
-  if ((n8 && !aligned16(Xq8)) || (n4 && !aligned16(Xq4)) || !aligned16(Wq) || !aligned16(Sx))
+  if ((n8 && !aligned16(Xq8)) || (n4 && !aligned16(Xq4)) || !aligned16(Wq) || !aligned16(Sx) || !aligned16(ws))
     return COMET_ERR_ALIGNMENT;
   int num_sms = 148;
   comet_status ds = device_check(&num_sms);
   if (ds != COMET_OK) return ds;
   Plan p = make_plan(M, N, K, num_sms);
   if (p.ws_bytes < 0) return COMET_ERR_SHAPE;
-  if (!Acc && p.ws_bytes > 0 && (ws == nullptr || (int64_t)ws_bytes < p.ws_bytes)) return COMET_ERR_WORKSPACE;
+  if (p.ws_bytes > 0 && (ws == nullptr || (int64_t)ws_bytes < p.ws_bytes)) return COMET_ERR_WORKSPACE;
 
-  CUtensorMap tmW, tmX4, tmX8;
-  // weights are tiled (8 KB contiguous slabs) and loaded with 1-D bulk copies;
-  // tmW is an unused placeholder map
-  if (!make_map_u8(&tmW, Wq, (uint64_t)K / 2, (uint64_t)N, (uint64_t)K / 2, 64, 128, CU_TENSOR_MAP_SWIZZLE_NONE))
-    return COMET_ERR_CUDA;
-  if (n4 && PfCfg::kXPre && p.two_sm && use_pf()) {
-    // pre-expanded INT4 token blocks (x16 INT8, staging byte order) in a
-    // cached device buffer, TMA-loaded as SW128 INT8 rows like the INT8 plane.
-    // EXPERIMENT ONLY (COMET_PF_XPRE, off by default): the process-wide buffer
-    // is neither thread- nor multi-stream-safe; a product version would take
-    // it from the caller's workspace
-    static void* xe = nullptr;
-    static size_t xe_bytes = 0;
-    const size_t need = (size_t)M * n4 * 128;
-    if (need > xe_bytes) {
-      if (xe) cudaFree(xe);
-      if (cudaMalloc(&xe, need) != cudaSuccess) { xe = nullptr; xe_bytes = 0; return COMET_ERR_CUDA; }
-      xe_bytes = need;
-    }
-    const int64_t n16 = (int64_t)M * n4 * 4;
-    expand_int4_tokens_kernel<<<4 * num_sms, 256, 0, st>>>(reinterpret_cast<const uint4*>(Xq4),
-                                                           reinterpret_cast<uint4*>(xe), n16);
-    comet_status ls = check_launch();
-    if (ls != COMET_OK) return ls;
-    if (!make_map_u8(&tmX4, xe, (uint64_t)n4 * 128, (uint64_t)M, (uint64_t)n4 * 128, 128, p.bn,
-                     CU_TENSOR_MAP_SWIZZLE_128B))
-      return COMET_ERR_CUDA;
-  } else if (n4) {
-    // the TMEM-A prefill kernel reads packed token rows per thread: 64B swizzle
-    // keeps those 16-byte loads conflict-free
-    if (!make_map_u8(&tmX4, Xq4, (uint64_t)n4 * 64, (uint64_t)M, (uint64_t)n4 * 64, 64, p.bn,
-                     (p.two_sm && use_pf()) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE))
-      return COMET_ERR_CUDA;
-  } else {
-    tmX4 = tmW;  // never dereferenced
-  }
+  // token operand maps: the INT8 plane (both kernels, SW128 rows of 128 B);
+  // INT4 tokens as the e4m3 plane prepared below (prefill, SW128 rows of
+  // 128 B) or the packed plane (decode, unswizzled rows of 64 B)
+  CUtensorMap tmXp, tmX8;
   if (n8) {
     if (!make_map_u8(&tmX8, Xq8, (uint64_t)n8 * 128, (uint64_t)M, (uint64_t)n8 * 128, 128, p.bn,
                      CU_TENSOR_MAP_SWIZZLE_128B))
-      return COMET_ERR_CUDA;
-  } else {
-    tmX8 = tmW;
+      return map_fail("Xq8");
   }
+  uint8_t* x4e = reinterpret_cast<uint8_t*>(ws) + kCounterBytes;
+  float* cx = reinterpret_cast<float*>(x4e + align256((int64_t)M * K));
+  if (n4 && p.two_sm) {
+    if (!make_map_u8(&tmXp, x4e, (uint64_t)n4 * 128, (uint64_t)M, (uint64_t)n4 * 128, 128, p.bn,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+      return map_fail("X4e");
+  } else if (n4) {
+    if (!make_map_u8(&tmXp, Xq4, (uint64_t)n4 * 64, (uint64_t)M, (uint64_t)n4 * 64, 64, p.bn,
+                     CU_TENSOR_MAP_SWIZZLE_NONE))
+      return map_fail("Xq4");
+  }
+  if (!n8) tmX8 = tmXp;  // never dereferenced
+  if (!n4) tmXp = tmX8;
   GemmArgs a;
   a.M = M;
   a.N = N;
@@ -427,12 +348,23 @@ comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, in
   a.Y = reinterpret_cast<__half*>(Y);
   a.Wq = reinterpret_cast<const uint8_t*>(Wq);
   a.Acc = Acc;
+  a.CX = cx;
   a.splits = p.splits;
   a.ws_counter = reinterpret_cast<int*>(ws);
   a.ws_partial = ws ? reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + kCounterBytes) : nullptr;
-  if (We && !aligned16(We)) return COMET_ERR_ALIGNMENT;
-  if (Acc) return launch_gemm<true>(tmW, tmX4, tmX8, map, a, p, st, We);
-  return launch_gemm<false>(tmW, tmX4, tmX8, map, a, p, st, We);
+  if (n4 && p.two_sm) {
+    // a4 for the tokens, once per call: INT4 plane -> e4m3 plane + corrections
+    const int64_t items = ldsx * n4 * 4;
+    int64_t grid = (items + 255) / 256;
+    if (grid > (int64_t)num_sms * 8) grid = (int64_t)num_sms * 8;
+    cudaError_t e = launch_pdl(prep_tokens_kernel, dim3((unsigned)grid), dim3(256), 0, st,
+                               reinterpret_cast<const uint8_t*>(Xq4), (int)M, n4, ldsx, x4e, cx);
+    if (e != cudaSuccess) return cuda_fail(e);
+    comet_status ls = check_launch();
+    if (ls != COMET_OK) return ls;
+  }
+  if (Acc) return launch_gemm<true>(tmXp, tmX8, map, a, p, st);
+  return launch_gemm<false>(tmXp, tmX8, map, a, p, st);
 }
 
 int64_t plane_bytes(int32_t M, int32_t K, const uint8_t* bits, int want) {
@@ -444,8 +376,6 @@ int64_t plane_bytes(int32_t M, int32_t K, const uint8_t* bits, int want) {
   }
   return want == 8 ? (int64_t)M * cnt * 128 : (int64_t)M * cnt * 64;
 }
-
-int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
 
 template <bool kBf16>
 comet_status quantize_act_impl(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
@@ -583,34 +513,14 @@ comet_status comet_w4ax_gemm(const int8_t* Xq8, const void* Xq4, const float* Sx
                      workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
-comet_status comet_w4ax_gemm_ex(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
-                                const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq, const void* We,
-                                const float* Sw, int32_t N, int32_t group, void* Y, int64_t ldy, void* workspace,
-                                size_t workspace_bytes, comet_stream_t stream) {
-  return gemm_common(Xq8, Xq4, Sx, ldsx, block_bits, M, K, Wq, Sw, N, group, Y, ldy, nullptr, workspace,
-                     workspace_bytes, reinterpret_cast<cudaStream_t>(stream), We);
-}
-
-comet_status comet_expand_weight(const void* Wq, int32_t N, int32_t K, void* We, comet_stream_t stream) {
-  if (N < 0 || K <= 0) return COMET_ERR_INVALID_ARG;
-  if (K % 128 || N % 128 || K > 65536) return COMET_ERR_SHAPE;
-  if (N == 0) return COMET_OK;
-  if (!Wq || !We) return COMET_ERR_INVALID_ARG;
-  if (!aligned16(Wq) || !aligned16(We)) return COMET_ERR_ALIGNMENT;
-  comet_status ds = device_check(nullptr);
-  if (ds != COMET_OK) return ds;
-  const int64_t items = (int64_t)N * (K / 32);
-  expand_weights_kernel<<<(unsigned)((items + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<const uint8_t*>(Wq), N, K, reinterpret_cast<uint4*>(We));
-  return check_launch();
-}
 
 comet_status comet_w4ax_gemm_acc_i32(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
                                      const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq,
-                                     const float* Sw, int32_t N, int32_t group, int32_t* Acc, comet_stream_t stream) {
+                                     const float* Sw, int32_t N, int32_t group, int32_t* Acc, void* workspace,
+                                     size_t workspace_bytes, comet_stream_t stream) {
   if (M > 0 && N > 0 && !Acc) return COMET_ERR_INVALID_ARG;
-  return gemm_common(Xq8, Xq4, Sx, ldsx, block_bits, M, K, Wq, Sw, N, group, nullptr, N, Acc, nullptr, 0,
-                     reinterpret_cast<cudaStream_t>(stream));
+  return gemm_common(Xq8, Xq4, Sx, ldsx, block_bits, M, K, Wq, Sw, N, group, nullptr, N, Acc, workspace,
+                     workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
 comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
@@ -680,6 +590,26 @@ comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K,
     if (e != cudaSuccess) return cuda_fail(e);
   }
   return COMET_OK;
+}
+
+comet_status comet_gather_shards(const void* Yall, int32_t P, int32_t M, int32_t per, int32_t N, void* Y,
+                                 int64_t ldy, comet_stream_t stream) {
+  if (P <= 0 || M < 0 || per < 0 || N < 0) return COMET_ERR_INVALID_ARG;
+  if (per % 128 || N % 128 || (int64_t)P * per < N || ldy < N || ldy % 8) return COMET_ERR_SHAPE;
+  if (M == 0 || N == 0) return COMET_OK;
+  if (!Yall || !Y) return COMET_ERR_INVALID_ARG;
+  if (!aligned16(Yall) || !aligned16(Y)) return COMET_ERR_ALIGNMENT;
+  int num_sms = 148;
+  comet_status ds = device_check(&num_sms);
+  if (ds != COMET_OK) return ds;
+  const int64_t items = (int64_t)P * M * (per / 8);
+  int64_t grid = (items + 255) / 256;
+  if (grid > (int64_t)num_sms * 16) grid = (int64_t)num_sms * 16;
+  cudaError_t e = launch_pdl(gather_shards_kernel, dim3((unsigned)grid), dim3(256), 0,
+                             reinterpret_cast<cudaStream_t>(stream), reinterpret_cast<const uint4*>(Yall), (int)P,
+                             (int)M, (int)per, (int)N, reinterpret_cast<uint4*>(Y), ldy);
+  if (e != cudaSuccess) return cuda_fail(e);
+  return check_launch();
 }
 
 const char* comet_status_str(comet_status s) {
@@ -856,8 +786,8 @@ int comet_debug_cta_times(int enable, unsigned long long* host, int n) {
 int comet_debug_role_cycles(unsigned long long* host16) {
   return cudaMemcpyFromSymbol(host16, g_role_cycles, sizeof(unsigned long long) * 16) == cudaSuccess ? 0 : -1;
 }
-int comet_debug_trace(unsigned long long* host1280) {  // 20 x 64 entries
-  return cudaMemcpyFromSymbol(host1280, g_trace, sizeof(unsigned long long) * 1280) == cudaSuccess ? 0 : -1;
+int comet_debug_trace(unsigned long long* host2048) {  // 32 x 64 entries
+  return cudaMemcpyFromSymbol(host2048, g_trace, sizeof(unsigned long long) * 2048) == cudaSuccess ? 0 : -1;
 }
 int64_t comet_launch_count(void) { return g_launches.load(); }
 

@@ -2,8 +2,8 @@
 // P:L321 §5):
 //   gemm_decode.cuh  M <= 128 tokens: swap-AB, weights as the TMEM A operand,
 //                    stream-K over (tile, K-block) units (HBM-bound regime);
-//   gemm_2sm.cuh     M > 128 tokens: persistent CTA-pair (cta_group::2) tiles
-//                    of 256 tokens x 256 weight rows (tensor-bound regime).
+//   gemm_pf.cuh      M > 128 tokens: persistent CTA-pair (cta_group::2) tiles
+//                    of 256 tokens x 192 weight rows (tensor-bound regime).
 #pragma once
 #include <cuda_fp16.h>
 #include <stdint.h>
@@ -22,6 +22,7 @@ struct GemmArgs {
   __half* Y;
   const uint8_t* Wq;  // tiled packed weights: slab (tile, block) at (tile * nb + block) * 8192
   int32_t* Acc;  // debug output (per-block INT32, logical units)
+  const float* CX;  // prefill: 8 * sum(xq) per (INT4 block rank, row) [n4 x ldsx]
   float* ws_partial;
   int* ws_counter;
   int splits;
@@ -82,7 +83,7 @@ struct RoleTimer {
 // (0 W issue, 1 X issue, 2 data arrived, 3 expanded, 4 MMA issued,
 //  5 accumulator ready, 6 accumulator released, 7 unit retired,
 //  8 epilogue iteration top, 9 epilogue scales ready)
-__device__ unsigned long long g_trace[20][64];
+__device__ unsigned long long g_trace[32][64];
 DEVI void trace(bool on, int ev, int i) {
   if (kTraceBuild && on && i < 64) g_trace[ev][i] = clk64();
 }

@@ -61,7 +61,8 @@ def test_size_helpers():
     bad = np.array([8, 5], np.uint8)
     assert L.comet_act_plane8_bytes(1, 256, bad.ctypes.data_as(ctypes.c_void_p)) == -1
     assert L.comet_w4ax_gemm_workspace_bytes(16, 100, 512) == -1  # N % 128
-    assert L.comet_w4ax_gemm_workspace_bytes(4096, 4096, 4096) == 0  # enough tiles: no split-K
+    # prefill: the tile counters + the e4m3 token plane (M*K at most) + corrections (K/128 x ldsx fp32)
+    assert L.comet_w4ax_gemm_workspace_bytes(4096, 4096, 4096) == 64 * 1024 + 4096 * 4096 + 32 * 4096 * 4
     assert L.comet_w4ax_gemm_workspace_bytes(16, 4096, 4096) > 64 * 1024  # decode: split-K partials
 
 

@@ -220,3 +220,32 @@ def trace2(M, N, K, n8, cta=0, steps=40):
     print("step " + " ".join(f"{n:>7s}" for n in names))
     for i in range(steps):
         print(f"{i:4d} " + " ".join(f"{a[e, i] - t0:7d}" for e in range(8)))
+
+
+def trace_pf(M, N, K, n8, cta=0, steps=64, group="K"):
+    """fp8-promotion prefill kernel (gemm_pf.cuh): per-block event timeline of one (leader) CTA"""
+    import ctypes
+    L = comet.lib()
+    L.comet_debug_cta_times.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
+    L.comet_debug_trace.argtypes = [ctypes.c_void_p]
+    buf = (ctypes.c_ulonglong * 2048)()
+    L.comet_debug_cta_times(cta + 1, None, 0)
+    run(M, N, K, n8, group, reps=1)
+    L.comet_debug_cta_times(0, None, 0)
+    L.comet_debug_trace(buf)
+    a = np.array(buf[:], dtype=np.int64).reshape(32, 64)
+    t0 = a[4, 0]
+    names = ["Ptop", "Ptfull", "Prel", "Pend", "Mtop", "Mrdy", "Mtemp", "Mcomm", "Stop", "Slfull", "Smdone",
+             "Srdy", "Wiss", "Xiss", "P19tf", "P19rel"]
+    print(f"M={M} N={N} K={K} g={group} CTA{cta} pf trace (cycles rel. first MMA-warp iteration):")
+    print("step " + " ".join(f"{n:>7s}" for n in names))
+    for i in range(steps):
+        print(f"{i:4d} " + " ".join(f"{a[e, i] - t0:7d}" for e in range(16)))
+    d = np.diff(a[7, 8:steps])
+    print(f"MMA commit interval steps 8..{steps - 1}: median {np.median(d):.0f} mean {d.mean():.0f} cycles")
+    print("MMA issue detail: temty, elected, after MMA0, after MMA3, after commit0, after commit1; then P19 tfull/release")
+    for i in range(8, 24):
+        print(f"  {i:3d} " + " ".join(f"{a[e, i] - t0:7d}" for e in (6, 16, 17, 18, 19, 7, 15)))
+    print("staging detail: mdone seen, LDS landed, weights stored, tokens st issued, proxy fence done, st wait done, ready arrived")
+    for i in range(8, 24):
+        print(f"  {i:3d} " + " ".join(f"{a[e, i] - t0:7d}" for e in (10, 20, 21, 22, 23, 24, 11)))
