@@ -405,7 +405,7 @@ comet_status quantize_act_impl(const void* X, int64_t ldx, int32_t M, int32_t K,
       cudaError_t e = cudaFuncSetAttribute(perm ? quantize_act_rows_kernel<true, false, kBf16> : quantize_act_rows_kernel<false, false, kBf16>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return cuda_fail(e);
-      int per_sm = (228 * 1024) / (smem + 1024);
+      int per_sm = (228 * 1024) / (smem + (int)sizeof(ScaleTab) + 1024);  // + the static scale table
       if (per_sm > 8) per_sm = 8;
       if (per_sm < 1) per_sm = 1;
       int64_t grid = (int64_t)num_sms * per_sm;
@@ -688,7 +688,7 @@ comet_status comet_quantize_act_static(const void* X, int64_t ldx, int32_t M, in
     cudaError_t e = cudaFuncSetAttribute(perm ? quantize_act_rows_kernel<true, true> : quantize_act_rows_kernel<false, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_fail(e);
-    int per_sm = (228 * 1024) / (smem + 1024);
+    int per_sm = (228 * 1024) / (smem + (int)sizeof(ScaleTab) + 1024);  // + the kernel's static scale table
     if (per_sm > 8) per_sm = 8;
     if (per_sm < 1) per_sm = 1;
     int num_sms = 148;

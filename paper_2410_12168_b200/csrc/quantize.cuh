@@ -42,6 +42,70 @@ DEVI void quant8(const float (&x)[8], float r, int32_t (&q)[8]) {
   for (int j = 0; j < 8; ++j) q[j] = round_half_away(__fmul_rn(x[j], r));
 }
 
+// ---- the fast dynamic path (row-staged kernel) ---------------------------
+// q = round_half_away(x * r) as the two's-complement bits of M + q in a float
+// (M = 1.5 * 2^23: the low byte of the result is q mod 256), without F2I:
+//   u = RZ(|v| + 0.5)  (RZ never rounds up to the next integer, so floor(u) ==
+//                       floor(|v| + 0.5); round-to-nearest would, for |v| just
+//                       below 0.5, where the sum lands in a coarser binade)
+//   t = RD(u + M)   = M + floor(u)            (one directed rounding, exact)
+//   k = t - M       = floor(|v| + 0.5)        (exact)
+//   M + copysign(k, v)                        (exact)
+// |v| <= qmax (1 + 2^-22) here (v = x * fl(qmax / a), |x| <= a), so q needs no clamp.
+DEVI uint32_t rha_bits(float v) {
+  const float M = 12582912.0f;
+  const float u = __fadd_rz(fabsf(v), 0.5f);
+  const float k = __fadd_rn(__fadd_rd(u, M), -M);
+  return __float_as_uint(__fadd_rn(copysignf(k, v), M));
+}
+// s = a / qmax and r = qmax / a (IEEE, as __fdiv_rn) for an a whose fp32
+// mantissa has at most 10 significant fraction bits (an fp16 or bf16 value):
+// a = 2^E * m with m in [1, 2), so a / qmax = 2^E * (m / qmax) and the
+// correctly rounded quotient is 2^E * RN(m / qmax) while it stays normal;
+// tab holds RN(m / qmax) and RN(qmax / m) for the 1024 mantissas (filled with
+// __fdiv_rn by the kernel).  Extreme exponents fall back to the division.
+struct ScaleTab {
+  float v[4][1024];  // s7, r7, s127, r127
+};
+DEVI void fill_scale_tab(ScaleTab* t) {
+  for (int i = threadIdx.x; i < 4 * 1024; i += blockDim.x) {
+    const int k = i >> 10, j = i & 1023;
+    const float m = 1.0f + (float)j * (1.0f / 1024.0f);
+    const float qm = k < 2 ? 7.0f : 127.0f;
+    t->v[k][j] = (k & 1) ? __fdiv_rn(qm, m) : __fdiv_rn(m, qm);
+  }
+}
+DEVI void scale_recip(float a, bool is8, const ScaleTab* t, float& s, float& r) {
+  const uint32_t ab = __float_as_uint(a);
+  const uint32_t ex = ab & 0x7F800000u;
+  if (a == 0.0f) {
+    s = 1.0f;
+    r = 0.0f;
+  } else if (ex >= 0x1A000000u && ex <= 0x64000000u && (ab & 0x1FFFu) == 0) {  // 2^-75 <= a < 2^73
+    const int k = is8 ? 2 : 0, j = (ab >> 13) & 1023;
+    const uint32_t d = ex - 0x3F800000u;
+    s = __uint_as_float(__float_as_uint(t->v[k][j]) + d);
+    r = __uint_as_float(__float_as_uint(t->v[k + 1][j]) - d);
+  } else {
+    const float qmax = is8 ? 127.0f : 7.0f;
+    s = __fdiv_rn(a, qmax);
+    r = __fdiv_rn(qmax, a);
+  }
+}
+// 8 values -> the O4 INT4 word (byte j = q_j & 0xF | (q_{j+4} & 0xF) << 4) or
+// two INT8 words, from rha_bits results
+DEVI uint32_t pack_int4_bits(const uint32_t (&h)[8]) {
+  const uint32_t lo = __byte_perm(__byte_perm(h[0], h[1], 0x0040), __byte_perm(h[2], h[3], 0x0040), 0x5410);
+  const uint32_t hi = __byte_perm(__byte_perm(h[4], h[5], 0x0040), __byte_perm(h[6], h[7], 0x0040), 0x5410);
+  uint32_t w;
+  asm("lop3.b32 %0, %1, %2, 0x0F0F0F0F, 0xD8;" : "=r"(w) : "r"(hi << 4), "r"(lo));  // (lo & m) | (hi<<4 & ~m)
+  return w;
+}
+DEVI uint2 pack_int8_bits(const uint32_t (&h)[8]) {
+  return make_uint2(__byte_perm(__byte_perm(h[0], h[1], 0x0040), __byte_perm(h[2], h[3], 0x0040), 0x5410),
+                    __byte_perm(__byte_perm(h[4], h[5], 0x0040), __byte_perm(h[6], h[7], 0x0040), 0x5410));
+}
+
 DEVI uint32_t pack_int4_word(const int32_t (&q)[8]) {
   uint32_t w = 0;
 #pragma unroll
@@ -154,7 +218,7 @@ DEVI void quant_item(const unsigned short* row, const unsigned short* psm, const
                      const BlockMap& map, int b, int o,
                      unsigned hmask, int64_t m, int64_t ldsx, int8_t* __restrict__ Xq8, int64_t ld8,
                      uint8_t* __restrict__ Xq4, int64_t ld4, float* __restrict__ Sx,
-                     const float* __restrict__ sstat = nullptr) {
+                     const float* __restrict__ sstat = nullptr, const ScaleTab* tab = nullptr) {
   const int i0 = b * 128 + o * 8;
   float x[8];
   if (kPerm && !COMET_Q_PERMSMEM) {
@@ -195,17 +259,23 @@ DEVI void quant_item(const unsigned short* row, const unsigned short* psm, const
       q[j] = fabsf(v) >= 8388608.0f ? (v > 0.0f ? qm : -qm) : min(qm, max(-qm, round_half_away(v)));
     }
   } else {
+    // dynamic scale: half-warp absmax, table-based IEEE s and r, F2I-free rounding
     float a = 0.0f;
 #pragma unroll
     for (int j = 0; j < 8; ++j) a = fmaxf(a, fabsf(x[j]));
 #pragma unroll
     for (int off = 8; off >= 1; off >>= 1) a = fmaxf(a, __shfl_xor_sync(hmask, a, off));
-    float r = 0.0f;
-    if (a != 0.0f) {
-      s = __fdiv_rn(a, qmax);
-      r = __fdiv_rn(qmax, a);
-    }
-    quant8(x, r, q);
+    float r;
+    scale_recip(a, is8, tab, s, r);
+    uint32_t h[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) h[j] = rha_bits(__fmul_rn(x[j], r));
+    if (is8)
+      *reinterpret_cast<uint2*>(Xq8 + m * ld8 + (int64_t)rank * 128 + o * 8) = pack_int8_bits(h);
+    else
+      *reinterpret_cast<uint32_t*>(Xq4 + m * ld4 + (int64_t)rank * 64 + o * 4) = pack_int4_bits(h);
+    if (o == 0) Sx[(int64_t)b * ldsx + m] = s;
+    return;
   }
   if (is8) {
     uint32_t lo = (uint32_t)(q[0] & 0xFF) | ((uint32_t)(q[1] & 0xFF) << 8) | ((uint32_t)(q[2] & 0xFF) << 16) |
@@ -240,6 +310,8 @@ __global__ void __launch_bounds__(256) quantize_act_rows_kernel(const __half* __
   grid_dep_launch();  // the GEMM that follows may get scheduled (PDL)
   const int K = nb * 128;
   __shared__ uint64_t rbar[kQNBuf];
+  __shared__ ScaleTab tab;
+  if (!kStatic) fill_scale_tab(&tab);
   const int half_id = threadIdx.x >> 4;
   const int o = threadIdx.x & 15;
   const unsigned hmask = 0xFFFFu << (threadIdx.x & 16);
@@ -274,10 +346,10 @@ __global__ void __launch_bounds__(256) quantize_act_rows_kernel(const __half* __
     const unsigned short* row = reinterpret_cast<const unsigned short*>(qsm + (size_t)buf * K * 2);
     int b = half_id;
     for (; b + 16 < nb; b += 32) {
-      quant_item<kPerm, kStatic, kBf16>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat);
-      quant_item<kPerm, kStatic, kBf16>(row, psm, perm, map, b + 16, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat);
+      quant_item<kPerm, kStatic, kBf16>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab);
+      quant_item<kPerm, kStatic, kBf16>(row, psm, perm, map, b + 16, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab);
     }
-    if (b < nb) quant_item<kPerm, kStatic, kBf16>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat);
+    if (b < nb) quant_item<kPerm, kStatic, kBf16>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab);
     __syncthreads();  // every half-warp is done with this buffer
   }
 }

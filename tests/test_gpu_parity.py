@@ -213,6 +213,44 @@ def test_fp16_extremes_quantize_bit_exact():
         assert np.array_equal(g[k].view(np.uint8), o[k].view(np.uint8)), k
 
 
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+def test_quantize_every_block_absmax_bit_exact(dtype):
+    """The row-staged quantizer derives s = a/qmax and r = qmax/a from a table
+    of the 1024 mantissas scaled by the exponent of a: sweep every positive
+    fp16 value (and a bf16 exponent range) as a block absmax, INT4 and INT8
+    blocks, planes and Sx bit-exact against the oracle's IEEE divisions."""
+    import importlib
+    rng = np.random.default_rng(11)
+    K = 1024
+    bits = np.array([4, 8, 4, 4, 8, 4, 4, 4], np.uint8)
+    if dtype == "fp16":
+        amax = np.arange(1, 0x7C00, dtype=np.uint16).view(np.float16).astype(np.float32)  # every finite positive fp16
+    else:
+        e = rng.integers(-100, 100, size=40000)
+        mant = rng.integers(0, 128, size=40000)
+        amax = ((1.0 + mant / 128.0) * 2.0 ** e).astype(np.float32)  # exact bf16 values
+    nitems = len(amax)
+    M = -(-nitems // 8)
+    a = np.resize(amax, M * 8).reshape(M, 8)
+    frac = rng.uniform(-1.0, 1.0, size=(M, 8, 128)).astype(np.float32)
+    X32 = frac * a[:, :, None]
+    X32[:, :, 0] = a  # the block absmax, exactly
+    X32 = X32.reshape(M, K)
+    bitsb = comet.BlockBits(bits)
+    if dtype == "fp16":
+        X = X32.astype(np.float16)
+        g8, g4, gs = comet.comet_quantize_act(to_dev(X), bitsb, None)
+        o8, o4, os_ = oracle.quantize_act(X, bits, None)
+    else:
+        O = importlib.import_module("oracle.fmpq_aux")
+        b16 = (X32.view(np.uint32) >> 16).astype(np.uint16)  # truncation: keeps the exact bf16 absmax
+        g8, g4, gs = comet.comet_quantize_act_bf16(to_dev(b16.view(np.int16)).view(torch.bfloat16), bitsb, None)
+        o8, o4, os_ = O.quantize_act_bf16(b16, bits)
+    torch.cuda.synchronize()
+    assert np.array_equal(g8.cpu().numpy(), o8) and np.array_equal(g4.cpu().numpy(), o4)
+    assert np.array_equal(gs.cpu().numpy().view(np.uint32), os_.view(np.uint32))
+
+
 def test_quantize_random_rows_bit_exact_large():
     """10^5-ish random rows across scales: planes and scales bit-exact."""
     rng = np.random.default_rng(77)
