@@ -70,9 +70,9 @@ def main(rnd):
           "(cold caches, serialised replays: durations are longer than the bench's "
           "CUDA-event numbers; compare shares and counters, not absolutes).", ""]
     traffic = {}
-    for tag, rep in [("prefill GEMM (LLaMA-2-7B, M=4096)", "prof_gemm_full"),
-                     ("quantize_act (LLaMA-2-7B, M=4096)", "prof_quant_full"),
-                     ("decode GEMM (LLaMA-3-70B, M=16)", "prof_decode_full")]:
+    for tag, rep in [("prefill GEMM (LLaMA-3-8B gate_up 28672x4096 and down 4096x14336, M=8192, per-channel weight scales)", "prof_gemm_full"),
+                     ("quantize_act (LLaMA-3-8B, M=8192; layers 2 and 3)", "prof_quant_full"),
+                     ("decode GEMM (LLaMA-3-70B, M=16; layers 2 and 3)", "prof_decode_full")]:
         path = os.path.join(OUT, rep + ".ncu-rep")
         if not os.path.exists(path):
             continue
@@ -93,12 +93,12 @@ def main(rnd):
             for i, k in enumerate(kernels):
                 rd, wr = k.get("dram__bytes_read.sum"), k.get("dram__bytes_write.sum")
                 if isinstance(rd, float) and isinstance(wr, float):
-                    traffic[f"layer{i}"] = rd + wr
+                    traffic[f"layer{i + 2}"] = rd + wr  # launches 0, 1 = layers 2 (gate_up), 3 (down)
     with open(os.path.join(PROF, f"ncu_summary_{rnd}.md"), "w") as f:
         f.write("\n".join(md) + "\n")
     if traffic:
         with open(os.path.join(PROF, "ncu_traffic.json"), "w") as f:
-            json.dump({"llama2-7b": traffic, "_note": "dram__bytes_read.sum + dram__bytes_write.sum per GEMM launch "
+            json.dump({"llama3-8b/gchannel": traffic, "_note": "dram__bytes_read.sum + dram__bytes_write.sum per GEMM launch "
                        "(bytes), from one ncu --set full capture (" + rnd + ")"}, f, indent=1)
     # launch list
     src = os.path.join(OUT, "launches.csv")
