@@ -11,8 +11,9 @@ blocks (3/32, 11/112), INT4 weights with per-output-channel scales
 (OmniQuant's W4A4 setting; 128-channel groups, are
 timed in the same run and reported under "alt_weight_scales"), seeded
 synthetic inputs (paper_2410_12168_b200.synth).  One step =
-one pass of the hot path over every layer: comet_quantize_act (a1+a2) +
-comet_w4ax_gemm (a3..a8) per layer; with N > 1 GPUs the weights are N-sharded
+one pass of the hot path over every layer through the whole-layer entry
+comet_w4ax_linear (device X and Y: a1+a2 quantize, a3..a8 GEMM; at prefill
+sizes its quantizer writes the GEMM's e4m3 token operand directly); with N > 1 GPUs the weights are N-sharded
 (tensor parallel), X is replicated, and each layer's Y shards are all-gathered
 (NCCL) and reassembled into Y [M x N] by comet_gather_shards inside the step.
 Weights are packed once before timing (a0 is offline); its time is
@@ -296,7 +297,7 @@ def run_comet(args, cfg, config_name):
                  Xh=torch.from_numpy(p["X"]).pin_memory(),
                  Yh=torch.empty((M, per), dtype=torch.float16).pin_memory(),
                  scratch=comet.new_workspace(comet.comet_w4ax_linear_scratch_bytes(M, per, K, bits), dev),
-                 ev=[], qev=[])
+                 ev=[], qev=[], lev=[])
         layers.append(L)
         del p
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
@@ -320,16 +321,23 @@ def run_comet(args, cfg, config_name):
                 comet.comet_gather_shards(yc, L["N"], out=L["Yfull"][m0:m1])
             return
         if timed:
-            qa, qb, gb = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            # per-kernel times: the two-call path (quantize, then the GEMM call = token prep + GEMM kernel)
+            qa, qb, gb, la, lb = (torch.cuda.Event(enable_timing=True) for _ in range(5))
             qa.record()
-        Xq8, Xq4, Sx = comet.comet_quantize_act(L["X"], L["bits"], L["perm"], out=L["planes"])
-        if timed:
+            Xq8, Xq4, Sx = comet.comet_quantize_act(L["X"], L["bits"], L["perm"], out=L["planes"])
             qb.record()
-        comet.comet_w4ax_gemm(Xq8, Xq4, Sx, L["bits"], Wq, Sw, grp, out=L["Y"], workspace=L["ws"])
-        if timed:
+            comet.comet_w4ax_gemm(Xq8, Xq4, Sx, L["bits"], Wq, Sw, grp, out=L["Y"], workspace=L["ws"])
             gb.record()
+            la.record()
+        # the step: the whole layer through comet_w4ax_linear (device X and Y): at prefill sizes its
+        # quantizer writes the GEMM's e4m3 token operand directly (no packed plane, no prep kernel)
+        comet.comet_w4ax_linear(L["X"], L["bits"], Wq, Sw, perm=L["perm"], group=grp, out=L["Y"],
+                                scratch=L["scratch"])
+        if timed:
+            lb.record()
             L["qev"].append((qa, qb))
             L["ev"].append((qb, gb))
+            L["lev"].append((la, lb))
         if world > 1:
             tp.all_gather_y(L["Y"], out=L["Yall"])
             comet.comet_gather_shards(L["Yall"], L["N"], out=L["Yfull"])
@@ -406,6 +414,7 @@ def run_comet(args, cfg, config_name):
         barrier()
     gemm_ms = [statistics.median(a.elapsed_time(b) for a, b in L["ev"]) if L["ev"] else None for L in layers]
     quant_ms = [statistics.median(a.elapsed_time(b) for a, b in L["qev"]) if L["qev"] else None for L in layers]
+    layer_ms = [statistics.median(a.elapsed_time(b) for a, b in L["lev"]) if L["lev"] else None for L in layers]
 
     # ---- the other weight-scale granularity ----
     alt = None
@@ -486,6 +495,9 @@ def run_comet(args, cfg, config_name):
            "tokens_per_s": M / (t_med * 1e-3),
            "gemm_us": [None if g is None else g * 1e3 for g in gemm_ms],
            "quantize_us": [None if q is None else q * 1e3 for q in quant_ms],
+           "layer_us": [None if q is None else q * 1e3 for q in layer_ms],
+           "kernel_times": ("gemm_us / quantize_us: a second eager pass of the two-call path (comet_quantize_act, "
+                            "comet_w4ax_gemm incl. its token prep kernel); layer_us: comet_w4ax_linear as in the step"),
            "quantize_hbm": {"achieved_gbs": [(2 * M * L["K"] + M * (128 * L["bits"].n8 + 64 * L["bits"].n4)
                                               + 4 * M * (L["K"] // 128)) / (q * 1e-3) / 1e9 if q else None
                                              for L, q in zip(layers, quant_ms)],

@@ -289,7 +289,10 @@ comet_status launch_gemm(const CUtensorMap& tmXp, const CUtensorMap& tmX8, const
 
 comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx, const uint8_t* bits,
                          int32_t M, int32_t K, const void* Wq, const float* Sw, int32_t N, int32_t group, void* Y,
-                         int64_t ldy, int32_t* Acc, void* ws, size_t ws_bytes, cudaStream_t st) {
+                         int64_t ldy, int32_t* Acc, void* ws, size_t ws_bytes, cudaStream_t st,
+                         bool prepared = false) {
+  // prepared (comet_w4ax_linear): the quantizer already wrote the prefill
+  // kernel's e4m3 token plane and corrections into the workspace (Xq4 unused)
   if (!bits || M < 0 || N < 0 || K <= 0) return COMET_ERR_INVALID_ARG;
   if (K % 128 || N % 128 || K > 65536) return COMET_ERR_SHAPE;
   if (group != 128 && group != K) return COMET_ERR_SHAPE;
@@ -303,7 +306,7 @@ comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, in
   if (Acc == nullptr && (ldy < N || ldy % 8)) return COMET_ERR_SHAPE;
   if (Acc == nullptr && ((reinterpret_cast<uintptr_t>(Y) & 15) || (reinterpret_cast<uintptr_t>(Sw) & 15)))
     return COMET_ERR_ALIGNMENT;
-  if ((n8 && !Xq8) || (n4 && !Xq4)) return COMET_ERR_INVALID_ARG;
+  if ((n8 && !Xq8) || (n4 && !Xq4 && !prepared)) return COMET_ERR_INVALID_ARG;
   if ((n8 && !aligned16(Xq8)) || (n4 && !aligned16(Xq4)) || !aligned16(Wq) || !aligned16(Sx) || !aligned16(ws))
     return COMET_ERR_ALIGNMENT;
   int num_sms = 148;
@@ -352,7 +355,7 @@ comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, in
   a.splits = p.splits;
   a.ws_counter = reinterpret_cast<int*>(ws);
   a.ws_partial = ws ? reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + kCounterBytes) : nullptr;
-  if (n4 && p.two_sm) {
+  if (n4 && p.two_sm && !prepared) {
     // a4 for the tokens, once per call: INT4 plane -> e4m3 plane + corrections
     const int64_t items = ldsx * n4 * 4;
     int64_t grid = (items + 255) / 256;
@@ -377,17 +380,19 @@ int64_t plane_bytes(int32_t M, int32_t K, const uint8_t* bits, int want) {
   return want == 8 ? (int64_t)M * cnt * 128 : (int64_t)M * cnt * 64;
 }
 
+// X4e/CX non-null: INT4 blocks go straight to the prefill GEMM's e4m3 operand
+// [M x n4*128 B] and its corrections (comet_w4ax_linear; row-staged kernel only)
 template <bool kBf16>
 comet_status quantize_act_impl(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
                                const uint8_t* block_bits, int8_t* Xq8, void* Xq4, float* Sx, int64_t ldsx,
-                               comet_stream_t stream) {
+                               comet_stream_t stream, uint8_t* X4e = nullptr, float* CX = nullptr) {
   if (M < 0 || K <= 0 || !block_bits) return COMET_ERR_INVALID_ARG;
   if (K % 128 || K > 65536 || ldx < K || ldx % 8 || ldsx < M || ldsx % 4) return COMET_ERR_SHAPE;
   BlockMap map;
   int n8 = 0, n4 = 0;
   if (!build_block_map(block_bits, K / 128, &map, &n8, &n4)) return COMET_ERR_INVALID_ARG;
   if (M == 0) return COMET_OK;
-  if (!X || !Sx || (n8 && !Xq8) || (n4 && !Xq4)) return COMET_ERR_INVALID_ARG;
+  if (!X || !Sx || (n8 && !Xq8) || (n4 && !Xq4 && !X4e)) return COMET_ERR_INVALID_ARG;
   if (!aligned16(X) || (n8 && !aligned16(Xq8)) || (n4 && !aligned16(Xq4)) || !aligned16(Sx) ||
       (perm && !aligned16(perm)))
     return COMET_ERR_ALIGNMENT;
@@ -400,27 +405,24 @@ comet_status quantize_act_impl(const void* X, int64_t ldx, int32_t M, int32_t K,
     // row-staged kernel: persistent CTAs, double-buffered rows in smem
     const int smem = kQNBuf * K * 2 + ((perm && COMET_Q_PERMSMEM) ? K * 2 : 0);  // row buffers + u16 permutation
     if (smem <= 200 * 1024) {
+      auto kern = X4e ? (perm ? quantize_act_rows_kernel<true, false, kBf16, true> : quantize_act_rows_kernel<false, false, kBf16, true>)
+                      : (perm ? quantize_act_rows_kernel<true, false, kBf16> : quantize_act_rows_kernel<false, false, kBf16>);
       // (dynamic smem above the 48 KB default needs the opt-in; set per call,
       // it is a cheap host-side attribute)
-      cudaError_t e = cudaFuncSetAttribute(perm ? quantize_act_rows_kernel<true, false, kBf16> : quantize_act_rows_kernel<false, false, kBf16>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return cuda_fail(e);
       int per_sm = (228 * 1024) / (smem + (int)sizeof(ScaleTab) + 1024);  // + the static scale table
       if (per_sm > 8) per_sm = 8;
       if (per_sm < 1) per_sm = 1;
       int64_t grid = (int64_t)num_sms * per_sm;
       if (grid > ldsx) grid = ldsx;
-      if (perm)
-        quantize_act_rows_kernel<true, false, kBf16><<<(int)grid, 256, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8,
-                                                                      (int64_t)n8 * 128, reinterpret_cast<uint8_t*>(Xq4),
-                                                                      (int64_t)n4 * 64, Sx);
-      else
-        quantize_act_rows_kernel<false, false, kBf16><<<(int)grid, 256, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8,
-                                                                       (int64_t)n8 * 128, reinterpret_cast<uint8_t*>(Xq4),
-                                                                       (int64_t)n4 * 64, Sx);
+      kern<<<(int)grid, 256, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
+                                         X4e ? X4e : reinterpret_cast<uint8_t*>(Xq4),
+                                         X4e ? (int64_t)n4 * 128 : (int64_t)n4 * 64, Sx, nullptr, CX);
       return check_launch();
     }
   }
+  if (X4e) return COMET_ERR_UNSUPPORTED;  // the fused output needs the row-staged kernel
   // one CTA per (8 rows, 2 blocks): 16 half-warp items
   const dim3 grid((unsigned)((ldsx + 7) / 8), (unsigned)((K / 128 + 1) / 2));
   if (perm)
@@ -578,10 +580,23 @@ comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K,
     Yd = p;
     ldyd = N;
   }
-  comet_status s = comet_quantize_act(Xd, ldxd, M, K, perm, block_bits, Xq8, Xq4, Sx, ldsx, stream);
-  if (s != COMET_OK) return s;
-  s = comet_w4ax_gemm(Xq8, Xq4, Sx, ldsx, block_bits, M, K, Wq, Sw, N, group, Yd, ldyd, ws,
-                      ws_bytes > 0 ? (size_t)ws_bytes : 0, stream);
+  comet_status s;
+  if (make_plan(M, N, K, 148).two_sm && (int64_t)kQNBuf * K * 2 <= 200 * 1024 && !COMET_Q_PERMSMEM) {
+    // prefill: the quantizer writes the GEMM's e4m3 token operand and its
+    // corrections straight into the workspace (no packed INT4 plane, no token
+    // preparation kernel); identical results to the two-call path
+    uint8_t* x4e = reinterpret_cast<uint8_t*>(ws) + kCounterBytes;
+    float* cx = reinterpret_cast<float*>(x4e + align256((int64_t)M * K));
+    s = quantize_act_impl<false>(Xd, ldxd, M, K, perm, block_bits, Xq8, nullptr, Sx, ldsx, stream, x4e, cx);
+    if (s != COMET_OK) return s;
+    s = gemm_common(Xq8, nullptr, Sx, ldsx, block_bits, M, K, Wq, Sw, N, group, Yd, ldyd, nullptr, ws,
+                    (size_t)ws_bytes, st, true);
+  } else {
+    s = comet_quantize_act(Xd, ldxd, M, K, perm, block_bits, Xq8, Xq4, Sx, ldsx, stream);
+    if (s != COMET_OK) return s;
+    s = comet_w4ax_gemm(Xq8, Xq4, Sx, ldsx, block_bits, M, K, Wq, Sw, N, group, Yd, ldyd, ws,
+                        ws_bytes > 0 ? (size_t)ws_bytes : 0, stream);
+  }
   if (s != COMET_OK) return s;
   if (y_host) {
     e = cudaMemcpy2DAsync(Y, (size_t)ldy * 2, Yd, (size_t)N * 2, (size_t)N * 2, (size_t)M, cudaMemcpyDeviceToHost, st);

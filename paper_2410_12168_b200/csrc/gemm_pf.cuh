@@ -65,40 +65,6 @@ DEVI void e4m3_offset_word(uint32_t w, uint32_t& lo, uint32_t& hi) {
   asm("lop3.b32 %0, %1, 0x0F0F0F0F, 0x08080808, 0x6A;" : "=r"(lo) : "r"(w));
   asm("lop3.b32 %0, %1, 0x0F0F0F0F, 0x08080808, 0x6A;" : "=r"(hi) : "r"(w >> 4));
 }
-// e4m3 of q * 2^-9 (sign-magnitude subnormal: byte = sign << 7 | |q|) for 4
-// two's-complement nibbles in the low half of each byte of L
-DEVI uint32_t e4m3_signed4(uint32_t L) {
-  const uint32_t S = L & 0x08080808u;  // sign bits
-  const uint32_t m1 = S >> 3;          // 1 per negative byte
-  return ((L ^ (m1 * 0x0Fu)) + m1) | (S << 4);  // |q| = 16 - n for a negative nibble n
-}
-
-// e4m3 of q * 2^-9 for the 8 values of one word of the sign-magnitude token
-// plane (prep_tokens_kernel): byte j holds |q_j| in bits 0-2, sign(q_j) in
-// bit 7, |q_{j+4}| in bits 4-6 and sign(q_{4+(j+3)%4}) in bit 3, so the low
-// four values are w & 0x87878787 and the high four the same mask of w rotated
-// right by 4 bits (one LOP3, one SHF, one LOP3 per 8 values)
-DEVI void e4m3_sm_word(uint32_t w, uint32_t& lo, uint32_t& hi) {
-  lo = w & 0x87878787u;
-  hi = __funnelshift_r(w, w, 4) & 0x87878787u;
-}
-
-template <bool kF8>
-DEVI void mma_ts_2sm(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
-  if (kF8)
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-        " tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-  else
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-        " tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-
 template <bool kF8>
 DEVI void mma_ss_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
   if (kF8)

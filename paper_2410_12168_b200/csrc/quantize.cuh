@@ -106,6 +106,23 @@ DEVI uint2 pack_int8_bits(const uint32_t (&h)[8]) {
                     __byte_perm(__byte_perm(h[4], h[5], 0x0040), __byte_perm(h[6], h[7], 0x0040), 0x5410));
 }
 
+// e4m3 of q * 2^-9 (sign-magnitude subnormal: byte = sign << 7 | |q|) for 4
+// two's-complement nibbles in the low half of each byte of L
+DEVI uint32_t e4m3_signed4(uint32_t L) {
+  const uint32_t S = L & 0x08080808u;  // sign bits
+  const uint32_t m1 = S >> 3;          // 1 per negative byte
+  return ((L ^ (m1 * 0x0Fu)) + m1) | (S << 4);  // |q| = 16 - n for a negative nibble n
+}
+// kE4 output of an INT4 block (the prefill GEMM's operand, written by the
+// quantizer in comet_w4ax_linear): 8 e4m3 bytes q * 2^-9 in K order and the
+// lane's sum of q (for the 8 * sum(xq) correction)
+DEVI uint2 e4m3_int4_bits(const uint32_t (&h)[8], int& qsum) {
+  const uint32_t lo = __byte_perm(__byte_perm(h[0], h[1], 0x0040), __byte_perm(h[2], h[3], 0x0040), 0x5410) & 0x0F0F0F0Fu;
+  const uint32_t hi = __byte_perm(__byte_perm(h[4], h[5], 0x0040), __byte_perm(h[6], h[7], 0x0040), 0x5410) & 0x0F0F0F0Fu;
+  qsum = __dp4a(lo + hi, 0x01010101u, 0u) - 2 * __dp4a((lo & 0x08080808u) + (hi & 0x08080808u), 0x01010101u, 0u);
+  return make_uint2(e4m3_signed4(lo), e4m3_signed4(hi));
+}
+
 DEVI uint32_t pack_int4_word(const int32_t (&q)[8]) {
   uint32_t w = 0;
 #pragma unroll
@@ -213,12 +230,16 @@ constexpr int kQNBuf = COMET_Q_NBUF;
 // kStatic (f4): the block's scale is the calibrated sstat[b]; q = clamp(rha(
 // fp32(x / s)), -qmax, qmax) (comet_quantize_act_static) instead of the
 // runtime absmax and the reciprocal multiply.
-template <bool kPerm, bool kStatic = false, bool kBf16 = false>
+// kE4: INT4 blocks are written as the prefill GEMM's e4m3 operand X4e
+// [M x n4*128 B] (ld4 = its row stride) plus CX[r4 * ldsx + m] = 8 sum(q)
+// instead of the packed plane (comet_w4ax_linear, see gemm_pf.cuh)
+template <bool kPerm, bool kStatic = false, bool kBf16 = false, bool kE4 = false>
 DEVI void quant_item(const unsigned short* row, const unsigned short* psm, const int32_t* __restrict__ gperm,
                      const BlockMap& map, int b, int o,
                      unsigned hmask, int64_t m, int64_t ldsx, int8_t* __restrict__ Xq8, int64_t ld8,
                      uint8_t* __restrict__ Xq4, int64_t ld4, float* __restrict__ Sx,
-                     const float* __restrict__ sstat = nullptr, const ScaleTab* tab = nullptr) {
+                     const float* __restrict__ sstat = nullptr, const ScaleTab* tab = nullptr,
+                     float* __restrict__ CX = nullptr) {
   const int i0 = b * 128 + o * 8;
   float x[8];
   if (kPerm && !COMET_Q_PERMSMEM) {
@@ -270,10 +291,17 @@ DEVI void quant_item(const unsigned short* row, const unsigned short* psm, const
     uint32_t h[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) h[j] = rha_bits(__fmul_rn(x[j], r));
-    if (is8)
+    if (is8) {
       *reinterpret_cast<uint2*>(Xq8 + m * ld8 + (int64_t)rank * 128 + o * 8) = pack_int8_bits(h);
-    else
+    } else if (kE4) {
+      int qs;
+      *reinterpret_cast<uint2*>(Xq4 + m * ld4 + (int64_t)rank * 128 + o * 8) = e4m3_int4_bits(h, qs);
+#pragma unroll
+      for (int off = 8; off >= 1; off >>= 1) qs += __shfl_xor_sync(hmask, qs, off);
+      if (o == 0) CX[(int64_t)rank * ldsx + m] = 8.0f * (float)qs;
+    } else {
       *reinterpret_cast<uint32_t*>(Xq4 + m * ld4 + (int64_t)rank * 64 + o * 4) = pack_int4_bits(h);
+    }
     if (o == 0) Sx[(int64_t)b * ldsx + m] = s;
     return;
   }
@@ -298,14 +326,15 @@ DEVI void quant_item(const unsigned short* row, const unsigned short* psm, const
 // global loads per lane.  Half-warp per (row, 128-channel block) item, lane =
 // 8 channels, two items in flight per half-warp; arithmetic and output
 // identical to quantize_act_kernel.
-template <bool kPerm, bool kStatic = false, bool kBf16 = false>
+template <bool kPerm, bool kStatic = false, bool kBf16 = false, bool kE4 = false>
 __global__ void __launch_bounds__(256) quantize_act_rows_kernel(const __half* __restrict__ X, int64_t ldx, int M,
                                                                 int nb, int64_t ldsx, const int32_t* __restrict__ perm,
                                                                 const __grid_constant__ BlockMap map,
                                                                 int8_t* __restrict__ Xq8, int64_t ld8,
                                                                 uint8_t* __restrict__ Xq4, int64_t ld4,
                                                                 float* __restrict__ Sx,
-                                                                const float* __restrict__ sstat = nullptr) {
+                                                                const float* __restrict__ sstat = nullptr,
+                                                                float* __restrict__ CX = nullptr) {
   extern __shared__ __align__(16) uint8_t qsm[];
   grid_dep_launch();  // the GEMM that follows may get scheduled (PDL)
   const int K = nb * 128;
@@ -334,7 +363,10 @@ __global__ void __launch_bounds__(256) quantize_act_rows_kernel(const __half* __
   for (int it = 0; m < ldsx; ++it, m += gridDim.x) {
     const int buf = it % kQNBuf;
     if (m >= M) {  // padding rows of the scale layout
-      for (int b = threadIdx.x; b < nb; b += blockDim.x) Sx[(int64_t)b * ldsx + m] = 1.0f;
+      for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        Sx[(int64_t)b * ldsx + m] = 1.0f;
+        if (kE4 && !(map.code[b] >> 15)) CX[(int64_t)(map.code[b] & 0x7FFF) * ldsx + m] = 0.0f;
+      }
       continue;
     }
     // prefetch row it + kQNBuf - 1 into the buffer row it - 1 used (its
@@ -346,10 +378,10 @@ __global__ void __launch_bounds__(256) quantize_act_rows_kernel(const __half* __
     const unsigned short* row = reinterpret_cast<const unsigned short*>(qsm + (size_t)buf * K * 2);
     int b = half_id;
     for (; b + 16 < nb; b += 32) {
-      quant_item<kPerm, kStatic, kBf16>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab);
-      quant_item<kPerm, kStatic, kBf16>(row, psm, perm, map, b + 16, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab);
+      quant_item<kPerm, kStatic, kBf16, kE4>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab, CX);
+      quant_item<kPerm, kStatic, kBf16, kE4>(row, psm, perm, map, b + 16, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab, CX);
     }
-    if (b < nb) quant_item<kPerm, kStatic, kBf16>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab);
+    if (b < nb) quant_item<kPerm, kStatic, kBf16, kE4>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab, CX);
     __syncthreads();  // every half-warp is done with this buffer
   }
 }

@@ -297,6 +297,23 @@ def test_linear_entry_with_host_buffers():
     assert np.array_equal(Yh.numpy().view(np.uint16), g["Y"].view(np.uint16))
 
 
+@pytest.mark.parametrize("M,group", [(301, 128), (517, 1024)])
+def test_linear_prefill_fused_quantizer(M, group):
+    """comet_w4ax_linear at prefill sizes: the quantizer writes the GEMM's e4m3
+    token operand and corrections directly (no packed plane, no prep kernel);
+    Y must be bit-identical to the two-call path (same tcgen05 arithmetic),
+    ragged M (ldsx padding rows), scattered INT8 blocks, both scale kinds."""
+    p = synth.make_problem(M, 640, 1024, n8=2, seed=31 + M, mask="scattered")
+    ref = gpu_path(p, group)["Y"]
+    W, perm, X = to_dev(p["W"]), to_dev(p["perm"]), to_dev(p["X"])
+    bits = comet.BlockBits(p["bits"])
+    Wq, Sw = comet.comet_pack_weight(W, perm, group)
+    scratch = comet.new_workspace(comet.comet_w4ax_linear_scratch_bytes(M, 640, 1024, bits), W.device)
+    Y = comet.comet_w4ax_linear(X, bits, Wq, Sw, perm=perm, group=group, scratch=scratch)
+    torch.cuda.synchronize()
+    assert np.array_equal(Y.cpu().numpy().view(np.uint16), ref.view(np.uint16))
+
+
 def test_linear_prefill_then_decode_same_scratch():
     """a prefill call (no GEMM workspace) must not overwrite the
     stream-K tile counters a later decode call on the same scratch uses."""
