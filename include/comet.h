@@ -198,6 +198,24 @@ comet_status comet_quantize_kv(const void* KV, int64_t ld, int32_t T, int32_t C,
 comet_status comet_dequantize_kv(const void* Q, const float* scale, const uint8_t* zp, int32_t T, int32_t C,
                                  int32_t group, void* out, int64_t ldo, comet_stream_t stream);
 
+/* ---- f3: attention over the KV4 cache ("dequant-in-attention") ----------
+ * One decode query per head (§3.2: the KV4 cache feeds the
+ * memory-bound activation-activation operator): for head h of H (D = 128
+ * channels each, C = 128 H),
+ *   o[h] = softmax_t(softmax_scale * q[h] . K^[t, h]) . V^[t, h]
+ * where K^, V^ = fp16_rn((q - zp) * scale) are the caches produced by
+ * comet_quantize_kv on [T x C] (Kq/Vq packed [T x C/2], Ks/Vs fp32 and Kz/Vz
+ * uint8 [ceil(T/group) x C]), dequantised on the fly (never written out).
+ * q: fp16 [H x 128]; out: fp16 [H x 128]; D must be 128.  workspace: DEVICE,
+ * at least comet_attention_kv4_workspace_bytes(T, H) bytes (per-split
+ * partials), 16-byte aligned; Ks/Vs 16-byte, Kz/Vz 4-byte aligned.  Softmax
+ * and sums in fp32 (expf), result rounded once to fp16. */
+int64_t comet_attention_kv4_workspace_bytes(int32_t T, int32_t H);
+comet_status comet_attention_kv4(const void* q, const void* Kq, const float* Ks, const uint8_t* Kz, const void* Vq,
+                                 const float* Vs, const uint8_t* Vz, int32_t T, int32_t H, int32_t D, int32_t group,
+                                 float softmax_scale, void* out, void* workspace, size_t workspace_bytes,
+                                 comet_stream_t stream);
+
 /* ---- f4: static per-block activation scales (SPEC
  * S:L157-165 "per-block QuantParams computed from the permuted channels'
  * pooled min/max at the block's bit width, symmetric scheme") ----

@@ -156,6 +156,36 @@ def dequantize_kv(q: np.ndarray, scale: np.ndarray, zp: np.ndarray, group: int) 
     return y.astype(np.float16)
 
 
+def unpack_kv(packed: np.ndarray) -> np.ndarray:
+    """[T x C/2] bytes -> [T x C] nibbles (inverse of pack_kv)."""
+    T, h = packed.shape
+    q = np.zeros((T, 2 * h), dtype=np.uint8)
+    q[:, 0::2] = packed & 0xF
+    q[:, 1::2] = packed >> 4
+    return q
+
+
+def attention_kv4(q: np.ndarray, K, V, group: int, softmax_scale: float, D: int = 128) -> np.ndarray:
+    """f3 dequant-in-attention (§3.2: the KV4 cache serves the
+    memory-bound activation-activation operator): one decode query per
+    head, K and V given as their KV4 caches (packed [T x C/2], scale [G x C],
+    zp [G x C]).  K^, V^ = dequantize_kv(...) (fp16, the values the cache
+    stands for); for head h: s_t = softmax_scale * sum_d q[h, d] K^[t, hD + d],
+    p = exp(s - max s) / sum exp(s - max s), o[h] = sum_t p_t V^[t, hD : hD + D].
+    Everything after the dequantisation in fp64; returns fp64 [H x D]."""
+    Kh = dequantize_kv(unpack_kv(K[0]), K[1], K[2], group).astype(np.float64)
+    Vh = dequantize_kv(unpack_kv(V[0]), V[1], V[2], group).astype(np.float64)
+    H = q.shape[0]
+    out = np.zeros((H, D), dtype=np.float64)
+    for h in range(H):
+        qh = q[h].astype(np.float64)
+        s = softmax_scale * (Kh[:, h * D:(h + 1) * D] @ qh)
+        e = np.exp(s - s.max())
+        p = e / e.sum()
+        out[h] = p @ Vh[:, h * D:(h + 1) * D]
+    return out
+
+
 # ------------------------------------------------------------------ f4 ----
 # Static per-block activation scales (SURVEY 8(f) f4; SPEC S:L157-165
 # assign_block_precision: "per-block QuantParams computed from the permuted

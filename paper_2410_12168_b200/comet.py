@@ -25,7 +25,8 @@ EXPORTS = ["comet_act_plane8_bytes", "comet_act_plane4_bytes", "comet_act_ldsx",
            "comet_w4ax_linear_scratch_bytes", "comet_pack_weight", "comet_quantize_act", "comet_w4ax_gemm",
            "comet_w4ax_gemm_acc_i32", "comet_w4ax_linear", "comet_calib_absmax", "comet_fmpq_map",
            "comet_quantize_kv", "comet_dequantize_kv", "comet_static_act_scales", "comet_quantize_act_static",
-           "comet_quantize_act_bf16", "comet_gather_shards",
+           "comet_quantize_act_bf16", "comet_gather_shards", "comet_attention_kv4",
+           "comet_attention_kv4_workspace_bytes",
            "comet_status_str", "comet_last_cuda_error",
            "comet_launch_count"]
 
@@ -79,6 +80,10 @@ def lib():
         L.comet_quantize_kv.restype = ctypes.c_int
         L.comet_dequantize_kv.argtypes = [P, P, P, i32, i32, i32, P, i64, P]
         L.comet_dequantize_kv.restype = ctypes.c_int
+        L.comet_attention_kv4_workspace_bytes.argtypes = [i32, i32]
+        L.comet_attention_kv4_workspace_bytes.restype = i64
+        L.comet_attention_kv4.argtypes = [P, P, P, P, P, P, P, i32, i32, i32, i32, ctypes.c_float, P, P, sz, P]
+        L.comet_attention_kv4.restype = ctypes.c_int
         L.comet_gather_shards.argtypes = [P, i32, i32, i32, i32, P, i64, P]
         L.comet_gather_shards.restype = ctypes.c_int
         L.comet_quantize_act_bf16.argtypes = [P, i64, i32, i32, P, P, P, P, P, i64, P]
@@ -305,6 +310,23 @@ def comet_w4ax_gemm(Xq8, Xq4, Sx, bits, Wq, Sw, group: int = BLOCK, out: Optiona
                                _ptr(workspace), 0 if workspace is None else workspace.numel(), _stream(stream))
     _check("comet_w4ax_gemm", st)
     return Y
+
+
+def comet_attention_kv4(q: torch.Tensor, K, V, group: int, softmax_scale: float, workspace=None, stream=None):
+    """f3: decode attention over KV4 caches (K, V: (Q packed [T x C/2], scale [G x C], zp [G x C]) from
+    comet_quantize_kv); q fp16 [H x 128] -> out fp16 [H x 128]."""
+    H, D = q.shape
+    Kq, Ks, Kz = K
+    Vq, Vs, Vz = V
+    T = Kq.shape[0]
+    need = int(lib().comet_attention_kv4_workspace_bytes(T, H))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 16), dtype=torch.uint8, device=q.device)
+    out = torch.empty((H, D), dtype=torch.float16, device=q.device)
+    st = lib().comet_attention_kv4(_ptr(q), _ptr(Kq), _ptr(Ks), _ptr(Kz), _ptr(Vq), _ptr(Vs), _ptr(Vz), T, H, D, group,
+                                   float(softmax_scale), _ptr(out), _ptr(workspace), workspace.numel(), _stream(stream))
+    _check("comet_attention_kv4", st)
+    return out
 
 
 def comet_gather_shards(Yall: torch.Tensor, N: int, out: Optional[torch.Tensor] = None, stream=None):

@@ -627,6 +627,39 @@ comet_status comet_gather_shards(const void* Yall, int32_t P, int32_t M, int32_t
   return check_launch();
 }
 
+int64_t comet_attention_kv4_workspace_bytes(int32_t T, int32_t H) {
+  if (T <= 0 || H <= 0) return -1;
+  return (int64_t)H * ((T + kAttChunk - 1) / kAttChunk) * kAttPart * 4;
+}
+
+comet_status comet_attention_kv4(const void* q, const void* Kq, const float* Ks, const uint8_t* Kz, const void* Vq,
+                                 const float* Vs, const uint8_t* Vz, int32_t T, int32_t H, int32_t D, int32_t group,
+                                 float softmax_scale, void* out, void* workspace, size_t workspace_bytes,
+                                 comet_stream_t stream) {
+  if (T < 0 || H <= 0 || group <= 0) return COMET_ERR_INVALID_ARG;
+  if (D != kAttD) return COMET_ERR_SHAPE;
+  if (T == 0) return COMET_OK;
+  if (!q || !Kq || !Ks || !Kz || !Vq || !Vs || !Vz || !out || !workspace) return COMET_ERR_INVALID_ARG;
+  if ((int64_t)workspace_bytes < comet_attention_kv4_workspace_bytes(T, H)) return COMET_ERR_WORKSPACE;
+  if (!aligned16(Ks) || !aligned16(Vs) || !aligned16(workspace) || (reinterpret_cast<uintptr_t>(Kz) & 3) ||
+      (reinterpret_cast<uintptr_t>(Vz) & 3) || (reinterpret_cast<uintptr_t>(Kq) & 1) ||
+      (reinterpret_cast<uintptr_t>(Vq) & 1) || (reinterpret_cast<uintptr_t>(q) & 1) ||
+      (reinterpret_cast<uintptr_t>(out) & 1))
+    return COMET_ERR_ALIGNMENT;
+  comet_status ds = device_check(nullptr);
+  if (ds != COMET_OK) return ds;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int S = (T + kAttChunk - 1) / kAttChunk;
+  float* part = reinterpret_cast<float*>(workspace);
+  attn_kv4_split_kernel<<<dim3((unsigned)H, (unsigned)S), 256, 0, st>>>(
+      reinterpret_cast<const __half*>(q), reinterpret_cast<const uint8_t*>(Kq), Ks, Kz,
+      reinterpret_cast<const uint8_t*>(Vq), Vs, Vz, T, H, group, softmax_scale, part);
+  comet_status ls = check_launch();
+  if (ls != COMET_OK) return ls;
+  attn_kv4_combine_kernel<<<(unsigned)H, kAttD, 0, st>>>(part, S, reinterpret_cast<__half*>(out));
+  return check_launch();
+}
+
 const char* comet_status_str(comet_status s) {
   switch (s) {
     case COMET_OK: return "COMET_OK";

@@ -226,4 +226,172 @@ __global__ void __launch_bounds__(256) quantize_act_static_kernel(const __half* 
   if (o == 0) Sx[(int64_t)b * ldsx + m] = s;
 }
 
+// ---- f3: dequant-in-attention over the KV4 cache (§3.2, §6.1) ----
+// One decode query per head: o_h = softmax(scale * q_h . K^_h^T) V^_h with
+// K^, V^ = fp16_rn((q - zp) * s) of the KV4 cache (the dequantisation
+// kv4_dequantize_kernel applies), never materialised in HBM: the cache is read
+// packed (0.5 B per element + its group parameters).  Split over tokens
+// (kAttChunk per CTA, flash-decoding style): each CTA writes (max, sum, o[128])
+// of its chunk, attn_kv4_combine_kernel merges the splits.  D = 128.
+constexpr int kAttD = 128;
+constexpr int kAttChunk = 512;  // tokens per CTA: 8 warps x 64 consecutive tokens
+constexpr int kAttPart = kAttD + 2;
+
+// 16 channels c .. c+15 of one token from a packed KV4 row (8 bytes, channel
+// pairs), dequantised and rounded to fp16 exactly as kv4_dequantize_kernel:
+// fp16_rn(fp32((n - zp) * s)); n - zp via the exact 2^23 magic (no I2F)
+struct Kv4Par {
+  float s[16];
+  float zf[16];  // 2^23 + zp
+};
+DEVI void kv4_load_par(const float* __restrict__ sc, const uint8_t* __restrict__ zp, int64_t off, Kv4Par& p) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float4 s4 = __ldg(reinterpret_cast<const float4*>(sc + off) + k);
+    p.s[4 * k] = s4.x; p.s[4 * k + 1] = s4.y; p.s[4 * k + 2] = s4.z; p.s[4 * k + 3] = s4.w;
+  }
+  const uint4 z = __ldg(reinterpret_cast<const uint4*>(zp + off));
+  const uint32_t zw[4] = {z.x, z.y, z.z, z.w};
+#pragma unroll
+  for (int j = 0; j < 16; ++j) p.zf[j] = 8388608.0f + (float)((zw[j >> 2] >> (8 * (j & 3))) & 0xFF);
+}
+DEVI void kv4_deq16(uint2 w, const Kv4Par& p, float (&v)[16]) {
+  const uint32_t ww[2] = {w.x, w.y};
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const uint32_t n = (ww[j >> 3] >> (4 * (j & 7))) & 0xF;
+    const float d = __fadd_rn(__uint_as_float(0x4B000000u | n), -p.zf[j]);  // n - zp, exact
+    v[j] = __half2float(__float2half_rn(__fmul_rn(d, p.s[j])));
+  }
+}
+
+// CTA = (head, chunk of kAttChunk tokens), 8 warps; a warp walks 64
+// consecutive tokens 4 at a time: lanes 8i .. 8i+7 hold token i of the four,
+// 16 channels each (one 8-byte load of the packed row), 3-step reduction per
+// token for the scores; the values pass keeps 16 running sums per lane.
+__global__ void __launch_bounds__(256) attn_kv4_split_kernel(const __half* __restrict__ q,
+                                                             const uint8_t* __restrict__ Kq,
+                                                             const float* __restrict__ Ks,
+                                                             const uint8_t* __restrict__ Kz,
+                                                             const uint8_t* __restrict__ Vq,
+                                                             const float* __restrict__ Vs,
+                                                             const uint8_t* __restrict__ Vz, int T, int H, int G,
+                                                             float scale, float* __restrict__ part) {
+  __shared__ float sc[kAttChunk];
+  __shared__ float red[8][kAttD];
+  __shared__ float wred[8];
+  const int h = blockIdx.x, split = blockIdx.y;
+  const int t0 = split * kAttChunk, t1 = min(T, t0 + kAttChunk);
+  const int C = H * kAttD;
+  const int64_t rowb = C / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane >> 3, cg = lane & 7;          // token of the four, channel group
+  const int c = h * kAttD + 16 * cg;                 // this lane's 16 channels
+  for (int i = threadIdx.x; i < kAttChunk; i += blockDim.x) sc[i] = -INFINITY;
+  float qv[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) qv[j] = __half2float(q[h * kAttD + 16 * cg + j]) * scale;
+  __syncthreads();
+  const int w0 = t0 + warp * 64, w1 = min(t1, w0 + 64);
+  Kv4Par par;
+  int g = -1;
+  for (int tb = w0; tb < w1; tb += 4) {
+    const int t = tb + sub;
+    float d = 0.f;
+    if (t < w1) {
+      if (t / G != g) {  // warp-divergent only across a group boundary
+        g = t / G;
+        kv4_load_par(Ks, Kz, (int64_t)g * C + c, par);
+      }
+      float k[16];
+      kv4_deq16(__ldg(reinterpret_cast<const uint2*>(Kq + (int64_t)t * rowb + (c >> 1))), par, k);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) d = fmaf(k[j], qv[j], d);
+    }
+#pragma unroll
+    for (int off = 4; off >= 1; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
+    if (cg == 0 && t < w1) sc[t - t0] = d;
+  }
+  __syncthreads();
+  float m = -INFINITY;
+  for (int i = threadIdx.x; i < kAttChunk; i += blockDim.x) m = fmaxf(m, sc[i]);
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if (lane == 0) wred[warp] = m;
+  __syncthreads();
+  m = wred[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) m = fmaxf(m, wred[w]);
+  __syncthreads();
+  float l = 0.f;
+  for (int i = threadIdx.x; i < kAttChunk; i += blockDim.x) {
+    const float p = t0 + i < t1 ? expf(sc[i] - m) : 0.f;
+    sc[i] = p;
+    l += p;
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+  if (lane == 0) wred[warp] = l;
+  __syncthreads();
+  float o[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) o[j] = 0.f;
+  g = -1;
+  for (int tb = w0; tb < w1; tb += 4) {
+    const int t = tb + sub;
+    if (t < w1) {
+      if (t / G != g) {
+        g = t / G;
+        kv4_load_par(Vs, Vz, (int64_t)g * C + c, par);
+      }
+      float v[16];
+      kv4_deq16(__ldg(reinterpret_cast<const uint2*>(Vq + (int64_t)t * rowb + (c >> 1))), par, v);
+      const float p = sc[t - t0];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) o[j] = fmaf(p, v[j], o[j]);
+    }
+  }
+  // the four token lanes of each channel group, then the warps
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    o[j] += __shfl_xor_sync(0xffffffffu, o[j], 8);
+    o[j] += __shfl_xor_sync(0xffffffffu, o[j], 16);
+  }
+  if (sub == 0) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) red[warp][16 * cg + j] = o[j];
+  }
+  __syncthreads();
+  float* dst = part + ((int64_t)h * gridDim.y + split) * kAttPart;
+  if (threadIdx.x < kAttD) {
+    float acc = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) acc += red[w][threadIdx.x];
+    dst[2 + threadIdx.x] = acc;
+  }
+  if (threadIdx.x == 0) {
+    float ls = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) ls += wred[w];
+    dst[0] = m;
+    dst[1] = ls;
+  }
+}
+
+// merge the splits of every head: o = sum_s e^(m_s - M) o_s / sum_s e^(m_s - M) l_s
+__global__ void __launch_bounds__(kAttD) attn_kv4_combine_kernel(const float* __restrict__ part, int S,
+                                                                 __half* __restrict__ out) {
+  const int h = blockIdx.x;
+  const float* p = part + (int64_t)h * S * kAttPart;
+  float M = -INFINITY;
+  for (int s = 0; s < S; ++s) M = fmaxf(M, p[s * kAttPart]);
+  float L = 0.f, o = 0.f;
+  for (int s = 0; s < S; ++s) {
+    const float e = expf(p[s * kAttPart] - M);
+    L = fmaf(e, p[s * kAttPart + 1], L);
+    o = fmaf(e, p[s * kAttPart + 2 + threadIdx.x], o);
+  }
+  out[h * kAttD + threadIdx.x] = __float2half_rn(o / L);
+}
+
 }  // namespace comet

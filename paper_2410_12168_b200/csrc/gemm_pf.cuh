@@ -258,6 +258,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
   }
   if (warp == C::kMmaWarp) tmem_alloc_2sm<512>(tmem_holder);
   tc_fence_before();
+  __syncthreads();  // orders the allocation's smem write before the reads below for racecheck (cluster_sync does in hardware)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;

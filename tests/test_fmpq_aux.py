@@ -119,6 +119,72 @@ def _lib_map(score, theta=8.0):
     return comet.comet_fmpq_map(score, theta)
 
 
+# ---------------------------------- f3: attention over the KV4 cache ----
+def _kv4_cache(T, C, G, rng, scale=1.0):
+    x = (rng.standard_normal((T, C)) * scale).astype(np.float16)
+    q, s, z = O.quantize_kv_vec(x, G)
+    return O.pack_kv(q), s, z
+
+
+def test_attention_kv4_single_token_returns_its_value():
+    # T = 1: the softmax of one score is 1, so o = V^[0] for any query
+    rng = np.random.default_rng(0)
+    K, V = _kv4_cache(1, 256, 128, rng), _kv4_cache(1, 256, 128, rng)
+    q = rng.standard_normal((2, 128)).astype(np.float16)
+    o = O.attention_kv4(q, K, V, 128, 0.088)
+    Vh = O.dequantize_kv(O.unpack_kv(V[0]), V[1], V[2], 128).astype(np.float64)
+    assert np.array_equal(o, Vh[0].reshape(2, 128))
+
+
+def test_attention_kv4_zero_query_is_the_mean_value():
+    # q = 0: every score is 0, the softmax is uniform, o = mean_t V^[t]
+    rng = np.random.default_rng(1)
+    T = 37
+    K, V = _kv4_cache(T, 128, 16, rng), _kv4_cache(T, 128, 16, rng)
+    o = O.attention_kv4(np.zeros((1, 128), np.float16), K, V, 16, 0.088)
+    Vh = O.dequantize_kv(O.unpack_kv(V[0]), V[1], V[2], 16).astype(np.float64)
+    assert np.allclose(o[0], Vh.mean(axis=0), rtol=0, atol=1e-12)
+
+
+def test_attention_kv4_dominant_key_selects_its_value():
+    # one key aligned with q and far larger than the rest: o -> V^[t*]
+    rng = np.random.default_rng(2)
+    T, C = 64, 128
+    x = (rng.standard_normal((T, C)) * 0.01).astype(np.float16)
+    x[17] = 4.0
+    qk, sk, zk = O.quantize_kv_vec(x, 64)
+    V = _kv4_cache(T, C, 64, rng)
+    q = np.full((1, 128), 1.0, np.float16)
+    o = O.attention_kv4(q, (O.pack_kv(qk), sk, zk), V, 64, 1.0)
+    Vh = O.dequantize_kv(O.unpack_kv(V[0]), V[1], V[2], 64).astype(np.float64)
+    assert np.allclose(o[0], Vh[17], rtol=0, atol=1e-9)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("T,H,G", [(1, 2, 128), (513, 4, 128), (3000, 8, 64), (700, 2, 32), (8192, 32, 128)])
+def test_attention_kv4_matches_oracle(T, H, G):
+    """GPU dequant-in-attention vs the fp64 oracle over the same KV4 caches:
+    |o - o_ref| <= 2^-10 |o_ref| + 2^-12 max|V^| (fp32 dot products, softmax
+    and sums in the kernel; one fp16 rounding of o)."""
+    import torch
+    from paper_2410_12168_b200 import comet
+    rng = np.random.default_rng(T + H)
+    C = 128 * H
+    xk = rng.standard_normal((T, C)).astype(np.float16)
+    xv = rng.standard_normal((T, C)).astype(np.float16)
+    xk[:, 5] = 0.75  # a constant channel (degenerate group rule)
+    q = rng.standard_normal((H, 128)).astype(np.float16)
+    dev = torch.device("cuda")
+    Kd = comet.comet_quantize_kv(torch.from_numpy(xk).to(dev), G)
+    Vd = comet.comet_quantize_kv(torch.from_numpy(xv).to(dev), G)
+    o = comet.comet_attention_kv4(torch.from_numpy(q).to(dev), Kd, Vd, G, 128 ** -0.5).float().cpu().numpy()
+    K = tuple(t.cpu().numpy() for t in Kd)
+    V = tuple(t.cpu().numpy() for t in Vd)
+    ref = O.attention_kv4(q, K, V, G, float(np.float32(128 ** -0.5)))
+    vmax = np.abs(O.dequantize_kv(O.unpack_kv(V[0]), V[1], V[2], G).astype(np.float64)).max()
+    assert np.all(np.abs(o - ref) <= 2.0 ** -10 * np.abs(ref) + 2.0 ** -12 * vmax)
+
+
 @pytest.mark.parametrize("seed", [0, 1, 2])
 def test_library_map_equals_oracle(seed):
     rng = np.random.default_rng(seed)

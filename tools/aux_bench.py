@@ -67,6 +67,16 @@ def main():
     out.append({"kernel": "quantize_act_static", "shape": [M, K], "us": t * 1e6, "GBs": byts / t / 1e9})
     t = timed(lambda: comet.comet_quantize_act(Xa, bits, perm, out=planes))
     out.append({"kernel": "quantize_act (dynamic)", "shape": [M, K], "us": t * 1e6, "GBs": byts / t / 1e9})
+    # f3: decode attention over KV4 caches (dequant-in-attention), 32 heads x 128, T tokens, group 128
+    for T in (8192, 32768):
+        H = 32
+        Kd = comet.comet_quantize_kv(torch.randn(T, H * 128, device="cuda").half(), 128)
+        Vd = comet.comet_quantize_kv(torch.randn(T, H * 128, device="cuda").half(), 128)
+        qh = torch.randn(H, 128, device="cuda").half()
+        ws = torch.empty(comet.lib().comet_attention_kv4_workspace_bytes(T, H), dtype=torch.uint8, device="cuda")
+        t = timed(lambda: comet.comet_attention_kv4(qh, Kd, Vd, 128, 128 ** -0.5, workspace=ws))
+        byts = 2 * (T * H * 64 + (T // 128) * H * 128 * 5)
+        out.append({"kernel": "attention_kv4", "shape": [T, H, 128], "us": t * 1e6, "GBs": byts / t / 1e9})
     for o in out:
         o["frac_of_hbm"] = o["GBs"] / pk
         print(json.dumps(o))
