@@ -151,12 +151,17 @@ comet_status comet_w4ax_gemm_acc_i32(const int8_t* Xq8, const void* Xq4, const f
                                      size_t workspace_bytes, comet_stream_t stream);
 
 /* ---- the whole linear layer (user call): quantize_act + w4ax_gemm ------
- * X and Y may be HOST (pinned or pageable) or DEVICE pointers; host buffers
- * are copied in/out on `stream` inside the call (X: M*ldx*2 bytes in, Y:
- * M*ldy*2 bytes out).  scratch: device memory of at least
- * comet_w4ax_linear_scratch_bytes(M, N, K, block_bits) bytes, first 64 KiB
- * zero on first use.  When Y is a host pointer the call synchronizes
- * `stream` before returning. */
+ * X and Y may be HOST (pinned or pageable) or DEVICE pointers.  Device X and
+ * Y: everything is enqueued on `stream`; at prefill sizes the quantizer
+ * writes the GEMM's e4m3 token operand directly (results identical to
+ * comet_quantize_act + comet_w4ax_gemm).  Host buffers: the rows are split
+ * into chunks (>= 1024 rows, at most 8) whose host->device copy, layer and
+ * device->host copy run as a pipeline on two library-internal copy streams
+ * ordered after the caller's earlier work on `stream` (X: M*K*2 bytes in,
+ * Y: M*N*2 bytes out); later work on `stream` is ordered after the copies.
+ * scratch: device memory of at least comet_w4ax_linear_scratch_bytes(M, N,
+ * K, block_bits) bytes, first 64 KiB zero on first use.  When Y is a host
+ * pointer the call synchronizes `stream` before returning. */
 comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
                                const uint8_t* block_bits, const void* Wq, const float* Sw, int32_t N, int32_t group,
                                void* Y, int64_t ldy, void* scratch, size_t scratch_bytes, comet_stream_t stream);

@@ -370,6 +370,37 @@ comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, in
   return launch_gemm<false>(tmXp, tmX8, map, a, p, st);
 }
 
+// comet_w4ax_linear with host buffers: two internal copy streams and their
+// events, created once per device and reused (thread-safe creation; one
+// host-buffer call at a time per device, which the call's final synchronize
+// already implies)
+constexpr int kLinMaxChunks = 8;
+struct LinStreams {
+  cudaStream_t in, out;
+  cudaEvent_t ev_start, ev_end, ev_end2, ev_in[kLinMaxChunks], ev_out[kLinMaxChunks];
+};
+LinStreams* lin_streams() {
+  static LinStreams g_ls[64];
+  static bool g_ok[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (!g_ok[dev]) {
+    LinStreams& L = g_ls[dev];
+    bool ok = cudaStreamCreateWithFlags(&L.in, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&L.out, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&L.ev_start, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&L.ev_end, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&L.ev_end2, cudaEventDisableTiming) == cudaSuccess;
+    for (int c = 0; c < kLinMaxChunks && ok; ++c)
+      ok = cudaEventCreateWithFlags(&L.ev_in[c], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&L.ev_out[c], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) return nullptr;
+    g_ok[dev] = true;
+  }
+  return &g_ls[dev];
+}
+
 int64_t plane_bytes(int32_t M, int32_t K, const uint8_t* bits, int want) {
   if (M < 0 || K <= 0 || K % 128 || !bits) return -1;
   int64_t cnt = 0;
@@ -554,56 +585,92 @@ comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K,
 
   char* p = reinterpret_cast<char*>(scratch);
   const int64_t ws_bytes = comet_w4ax_gemm_workspace_bytes(M, N, K);
-  void* ws = ws_bytes > 0 ? p : nullptr;  // counters stay at the scratch base (zeroed once, reset by the kernel)
+  void* ws = p;  // counters stay at the scratch base (zeroed once, reset by the kernels)
   p += align256(std::max<int64_t>(ws_bytes, kCounterBytes));
   const int64_t p8 = plane_bytes(M, K, block_bits, 8), p4 = plane_bytes(M, K, block_bits, 4);
   int8_t* Xq8 = reinterpret_cast<int8_t*>(p);
   p += align256(p8);
   void* Xq4 = p;
   p += align256(p4);
-  const int64_t ldsx = comet_act_ldsx(M);
   float* Sx = reinterpret_cast<float*>(p);
-  p += align256((K / 128) * ldsx * 4);
-  const void* Xd = X;
-  int64_t ldxd = ldx;
-  if (x_host) {  // stage the host rows densely (ld = K) in scratch
-    void* xs = p;
+  p += align256((K / 128) * comet_act_ldsx(M) * 4);
+  char* xs = nullptr;  // host X staged densely (ld = K)
+  if (x_host) {
+    xs = p;
     p += align256((int64_t)M * K * 2);
-    e = cudaMemcpy2DAsync(xs, (size_t)K * 2, X, (size_t)ldx * 2, (size_t)K * 2, (size_t)M, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(e);
-    Xd = xs;
-    ldxd = K;
   }
-  void* Yd = Y;
-  int64_t ldyd = ldy;
-  if (y_host) {
-    Yd = p;
-    ldyd = N;
-  }
-  comet_status s;
-  if (make_plan(M, N, K, 148).two_sm && (int64_t)kQNBuf * K * 2 <= 200 * 1024 && !COMET_Q_PERMSMEM) {
-    // prefill: the quantizer writes the GEMM's e4m3 token operand and its
-    // corrections straight into the workspace (no packed INT4 plane, no token
-    // preparation kernel); identical results to the two-call path
-    uint8_t* x4e = reinterpret_cast<uint8_t*>(ws) + kCounterBytes;
-    float* cx = reinterpret_cast<float*>(x4e + align256((int64_t)M * K));
-    s = quantize_act_impl<false>(Xd, ldxd, M, K, perm, block_bits, Xq8, nullptr, Sx, ldsx, stream, x4e, cx);
+  char* ys = y_host ? p : nullptr;  // host Y staged densely (ld = N)
+
+  // one device-resident layer over rows [m0, m0 + mc): quantize + GEMM on st
+  auto layer = [&](const void* Xd, int64_t ldxd, int32_t mc, void* Yd, int64_t ldyd) -> comet_status {
+    const int64_t ldsx = comet_act_ldsx(mc);
+    const int64_t wsb = comet_w4ax_gemm_workspace_bytes(mc, N, K);
+    if (make_plan(mc, N, K, 148).two_sm && (int64_t)kQNBuf * K * 2 <= 200 * 1024 && !COMET_Q_PERMSMEM) {
+      // prefill: the quantizer writes the GEMM's e4m3 token operand and its
+      // corrections straight into the workspace (no packed INT4 plane, no token
+      // preparation kernel); identical results to the two-call path
+      uint8_t* x4e = reinterpret_cast<uint8_t*>(ws) + kCounterBytes;
+      float* cx = reinterpret_cast<float*>(x4e + align256((int64_t)mc * K));
+      comet_status s = quantize_act_impl<false>(Xd, ldxd, mc, K, perm, block_bits, Xq8, nullptr, Sx, ldsx, stream,
+                                                x4e, cx);
+      if (s != COMET_OK) return s;
+      return gemm_common(Xq8, nullptr, Sx, ldsx, block_bits, mc, K, Wq, Sw, N, group, Yd, ldyd, nullptr, ws,
+                         (size_t)wsb, st, true);
+    }
+    comet_status s = comet_quantize_act(Xd, ldxd, mc, K, perm, block_bits, Xq8, Xq4, Sx, ldsx, stream);
     if (s != COMET_OK) return s;
-    s = gemm_common(Xq8, nullptr, Sx, ldsx, block_bits, M, K, Wq, Sw, N, group, Yd, ldyd, nullptr, ws,
-                    (size_t)ws_bytes, st, true);
-  } else {
-    s = comet_quantize_act(Xd, ldxd, M, K, perm, block_bits, Xq8, Xq4, Sx, ldsx, stream);
+    return comet_w4ax_gemm(Xq8, Xq4, Sx, ldsx, block_bits, mc, K, Wq, Sw, N, group, Yd, ldyd, ws,
+                           wsb > 0 ? (size_t)wsb : 0, stream);
+  };
+
+  if (!x_host && !y_host) return layer(X, ldx, M, Y, ldy);
+
+  // host buffers: row chunks pipeline H2D (copy stream) / compute (stream) /
+  // D2H (copy stream), so the PCIe transfers in both directions overlap the
+  // layer and each other; chunks of >= 1024 rows keep the prefill kernel's
+  // tiles full (a tail under 256 rows joins the previous chunk)
+  LinStreams* ls = lin_streams();
+  if (!ls) return cuda_fail(cudaGetLastError());
+  int nch = M >= 2048 ? std::min<int>(kLinMaxChunks, (int)((M + 1023) / 1024)) : 1;
+  std::vector<int> edges(nch + 1);
+  for (int c = 0; c <= nch; ++c) edges[c] = (int)(((int64_t)M * c / nch + 255) / 256 * 256);
+  edges[nch] = M;
+  e = cudaEventRecord(ls->ev_start, st);  // the copies follow the caller's earlier work on st
+  if (e != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaStreamWaitEvent(ls->in, ls->ev_start, 0)) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaStreamWaitEvent(ls->out, ls->ev_start, 0)) != cudaSuccess) return cuda_fail(e);
+  for (int c = 0; c < nch; ++c) {
+    const int m0 = edges[c], mc = edges[c + 1] - m0;
+    if (mc <= 0) continue;
+    const void* Xd = reinterpret_cast<const char*>(X) + (int64_t)m0 * ldx * 2;
+    int64_t ldxd = ldx;
+    if (x_host) {
+      e = cudaMemcpy2DAsync(xs + (int64_t)m0 * K * 2, (size_t)K * 2, Xd, (size_t)ldx * 2, (size_t)K * 2, (size_t)mc,
+                            cudaMemcpyHostToDevice, ls->in);
+      if (e != cudaSuccess) return cuda_fail(e);
+      if ((e = cudaEventRecord(ls->ev_in[c], ls->in)) != cudaSuccess) return cuda_fail(e);
+      if ((e = cudaStreamWaitEvent(st, ls->ev_in[c], 0)) != cudaSuccess) return cuda_fail(e);
+      Xd = xs + (int64_t)m0 * K * 2;
+      ldxd = K;
+    }
+    void* Yd = y_host ? static_cast<void*>(ys + (int64_t)m0 * N * 2)
+                      : static_cast<void*>(reinterpret_cast<char*>(Y) + (int64_t)m0 * ldy * 2);
+    comet_status s = layer(Xd, ldxd, mc, Yd, y_host ? N : ldy);
     if (s != COMET_OK) return s;
-    s = comet_w4ax_gemm(Xq8, Xq4, Sx, ldsx, block_bits, M, K, Wq, Sw, N, group, Yd, ldyd, ws,
-                        ws_bytes > 0 ? (size_t)ws_bytes : 0, stream);
+    if (y_host) {
+      if ((e = cudaEventRecord(ls->ev_out[c], st)) != cudaSuccess) return cuda_fail(e);
+      if ((e = cudaStreamWaitEvent(ls->out, ls->ev_out[c], 0)) != cudaSuccess) return cuda_fail(e);
+      e = cudaMemcpy2DAsync(reinterpret_cast<char*>(Y) + (int64_t)m0 * ldy * 2, (size_t)ldy * 2, Yd, (size_t)N * 2,
+                            (size_t)N * 2, (size_t)mc, cudaMemcpyDeviceToHost, ls->out);
+      if (e != cudaSuccess) return cuda_fail(e);
+    }
   }
-  if (s != COMET_OK) return s;
-  if (y_host) {
-    e = cudaMemcpy2DAsync(Y, (size_t)ldy * 2, Yd, (size_t)N * 2, (size_t)N * 2, (size_t)M, cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) return cuda_fail(e);
-    e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return cuda_fail(e);
-  }
+  // later work on st orders after the copies; host Y is complete on return
+  if ((e = cudaEventRecord(ls->ev_end, ls->out)) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaStreamWaitEvent(st, ls->ev_end, 0)) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaEventRecord(ls->ev_end2, ls->in)) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaStreamWaitEvent(st, ls->ev_end2, 0)) != cudaSuccess) return cuda_fail(e);
+  if (y_host && (e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e);
   return COMET_OK;
 }
 

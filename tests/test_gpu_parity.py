@@ -314,6 +314,23 @@ def test_linear_prefill_fused_quantizer(M, group):
     assert np.array_equal(Y.cpu().numpy().view(np.uint16), ref.view(np.uint16))
 
 
+def test_linear_host_buffers_pipelined_chunks():
+    """Host X and Y at M >= 2048: the call pipelines row chunks (H2D / layer /
+    D2H on internal copy streams); Y must equal the device-buffer call."""
+    M, N, K = 2600, 640, 1024
+    p = synth.make_problem(M, N, K, n8=2, seed=41, mask="scattered")
+    W, perm = to_dev(p["W"]), to_dev(p["perm"])
+    bits = comet.BlockBits(p["bits"])
+    Wq, Sw = comet.comet_pack_weight(W, perm, 128)
+    scratch = comet.new_workspace(comet.comet_w4ax_linear_scratch_bytes(M, N, K, bits), W.device)
+    Yd = comet.comet_w4ax_linear(to_dev(p["X"]), bits, Wq, Sw, perm=perm, scratch=scratch)
+    torch.cuda.synchronize()
+    Xh = torch.from_numpy(p["X"]).pin_memory()
+    Yh = torch.empty((M, N), dtype=torch.float16).pin_memory()
+    comet.comet_w4ax_linear(Xh, bits, Wq, Sw, perm=perm, out=Yh, scratch=scratch)
+    assert np.array_equal(Yh.numpy().view(np.uint16), Yd.cpu().numpy().view(np.uint16))
+
+
 def test_linear_prefill_then_decode_same_scratch():
     """a prefill call (no GEMM workspace) must not overwrite the
     stream-K tile counters a later decode call on the same scratch uses."""
