@@ -203,6 +203,26 @@ comet_status comet_quantize_kv(const void* KV, int64_t ld, int32_t T, int32_t C,
 comet_status comet_dequantize_kv(const void* Q, const float* scale, const uint8_t* zp, int32_t T, int32_t C,
                                  int32_t group, void* out, int64_t ldo, comet_stream_t stream);
 
+/* ---- f4: FP16 weight-scale storage ("the group size is 128 and each
+ * group has one FP16 scale factor") ------------------------
+ * comet_pack_weight_f16s: as comet_pack_weight (same Wq tiled layout, group
+ *   in {128, K}) but the scale of (row n, group j) is stored as fp16 and is
+ *   the one the weights are quantized with: a = max |w| over the group,
+ *   s = fp16_rn(fp32(a / 7)) (a == 0 -> 1; a nonzero s that underflows ->
+ *   2^-24), q = clamp(rha(fp32(w / s)), -7, 7).  Sw16: DEVICE fp16 [K/group x N].
+ * comet_w4ax_gemm_f16s: comet_w4ax_gemm with fp16 weight scales (stored at
+ *   half the bytes, widened to fp32 per call into the workspace: at least
+ *   comet_w4ax_gemm_f16s_workspace_bytes(M, N, K, group) bytes, first 64 KiB
+ *   zero on first use).  Results equal comet_w4ax_gemm on the fp32 values of
+ *   the fp16 scales. */
+comet_status comet_pack_weight_f16s(const void* W, int64_t ldw, int32_t N, int32_t K, const int32_t* perm,
+                                    int32_t group, void* Wq, void* Sw16, comet_stream_t stream);
+int64_t comet_w4ax_gemm_f16s_workspace_bytes(int32_t M, int32_t N, int32_t K, int32_t group);
+comet_status comet_w4ax_gemm_f16s(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
+                                  const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq, const void* Sw16,
+                                  int32_t N, int32_t group, void* Y, int64_t ldy, void* workspace,
+                                  size_t workspace_bytes, comet_stream_t stream);
+
 /* ---- f3: attention over the KV4 cache ("dequant-in-attention") ----------
  * One decode query per head (§3.2: the KV4 cache feeds the
  * memory-bound activation-activation operator): for head h of H (D = 128

@@ -250,6 +250,44 @@ def quantize_act_static(X: np.ndarray, bits, scales: np.ndarray, perm=None, k: i
     return Xq8, Xq4, Sx
 
 
+# f4 variant: FP16 weight-scale storage (the group-wise "one FP16 scale
+# factor" per group of 128 of the W4A8KV4 baseline; SURVEY 8(f) f4
+# "FP16/BF16 scale storage").  Per (output channel n, group j of the permuted
+# K axis): a = max |w|; s = fp16_rn(fp32(a / 7)) (a == 0 -> 1; a nonzero scale
+# that rounds below the smallest fp16 subnormal -> 2^-24); q = clamp(rha(fp32(
+# w / fp32(s))), -7, 7) (the stored scale is the one the weights are
+# quantized with, so dequantisation needs no other scale; the clamp catches
+# |w / s| up to 7.5 + when fp16 rounding made s < a / 7).  Sw16 [K/group x N]
+# fp16, Wq in the O4 nibble order.
+def pack_weight_f16s(W: np.ndarray, group: int = BLOCK, perm=None):
+    from . import pack_int4
+
+    W = np.asarray(W, dtype=np.float16)
+    N, K = W.shape
+    order = np.arange(K) if perm is None else np.asarray(perm, dtype=np.int64)
+    Wp = W.astype(np.float32)[:, order]
+    ng = K // group
+    Wq = np.zeros((N, K // 2), np.uint8)
+    Sw = np.zeros((ng, N), np.float16)
+    for n in range(N):
+        row = np.zeros(K, np.int8)
+        for j in range(ng):
+            g = Wp[n, j * group:(j + 1) * group]
+            a = np.float32(np.max(np.abs(g)))
+            if a == 0:
+                s = np.float16(1.0)
+            else:
+                s = np.float16(np.float32(a / np.float32(7.0)))
+                if s == 0:
+                    s = np.float16(2.0 ** -24)
+            Sw[j, n] = s
+            sf = np.float32(s)
+            for i in range(group):
+                row[j * group + i] = _q_static(g[i], sf, 7)
+        Wq[n] = pack_int4(row)
+    return Wq, Sw
+
+
 # f4 variant: bf16 activations.  A bf16 value's bits shifted left by 16 are
 # its fp32 encoding (exact); from there the quantization is O3 (the C
 # oracle's oracle_quantize_block, via oracle.quantize_block) on the permuted

@@ -694,6 +694,68 @@ comet_status comet_gather_shards(const void* Yall, int32_t P, int32_t M, int32_t
   return check_launch();
 }
 
+// ---- f4: FP16 weight-scale storage ---------------------------------------
+comet_status comet_pack_weight_f16s(const void* W, int64_t ldw, int32_t N, int32_t K, const int32_t* perm,
+                                    int32_t group, void* Wq, void* Sw16, comet_stream_t stream) {
+  if (N < 0 || K <= 0) return COMET_ERR_INVALID_ARG;
+  if (K % 128 || K > 65536 || N % 128 || (group != 128 && group != K) || ldw < K || ldw % 8) return COMET_ERR_SHAPE;
+  if (N == 0) return COMET_OK;
+  if (!W || !Wq || !Sw16) return COMET_ERR_INVALID_ARG;
+  if (!aligned16(W) || !aligned16(Wq) || (perm && !aligned16(perm)) || (reinterpret_cast<uintptr_t>(Sw16) & 1))
+    return COMET_ERR_ALIGNMENT;
+  comet_status ds = device_check(nullptr);
+  if (ds != COMET_OK) return ds;
+  const int64_t items = (int64_t)N * (K / group);
+  const unsigned grid = (unsigned)((items + 7) / 8);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const __half* Wh = reinterpret_cast<const __half*>(W);
+  if (perm)
+    pack_weight_f16s_kernel<true><<<grid, 256, 0, st>>>(Wh, ldw, N, K, group, perm, reinterpret_cast<uint8_t*>(Wq),
+                                                         reinterpret_cast<__half*>(Sw16));
+  else
+    pack_weight_f16s_kernel<false><<<grid, 256, 0, st>>>(Wh, ldw, N, K, group, perm, reinterpret_cast<uint8_t*>(Wq),
+                                                          reinterpret_cast<__half*>(Sw16));
+  return check_launch();
+}
+
+int64_t comet_w4ax_gemm_f16s_workspace_bytes(int32_t M, int32_t N, int32_t K, int32_t group) {
+  const int64_t base = comet_w4ax_gemm_workspace_bytes(M, N, K);
+  if (base < 0 || group <= 0 || K % group) return -1;
+  return align256(std::max<int64_t>(base, kCounterBytes)) + align256((int64_t)(K / group) * N * 4);
+}
+
+comet_status comet_w4ax_gemm_f16s(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
+                                  const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq, const void* Sw16,
+                                  int32_t N, int32_t group, void* Y, int64_t ldy, void* workspace,
+                                  size_t workspace_bytes, comet_stream_t stream) {
+  if (M < 0 || N < 0 || K <= 0 || !block_bits) return COMET_ERR_INVALID_ARG;
+  if (K % 128 || N % 128 || (group != 128 && group != K)) return COMET_ERR_SHAPE;
+  if (M == 0 || N == 0) return COMET_OK;
+  if (!Sw16 || !workspace) return COMET_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(Sw16) & 1) || !aligned16(workspace)) return COMET_ERR_ALIGNMENT;
+  const int64_t need = comet_w4ax_gemm_f16s_workspace_bytes(M, N, K, group);
+  if (need < 0 || (int64_t)workspace_bytes < need) return COMET_ERR_WORKSPACE;
+  const int64_t base = align256(std::max<int64_t>(comet_w4ax_gemm_workspace_bytes(M, N, K), kCounterBytes));
+  float* sw32 = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + base);
+  // validate the GEMM's own arguments first (no launch on a failing call)
+  if (ldsx < M || ldsx % 4 || ldy < N || ldy % 8) return COMET_ERR_SHAPE;
+  if (!Y || !Wq || !Sx) return COMET_ERR_INVALID_ARG;
+  int num_sms = 148;
+  comet_status ds = device_check(&num_sms);
+  if (ds != COMET_OK) return ds;
+  const int64_t n = (int64_t)(K / group) * N;
+  int64_t grid = (n + 255) / 256;
+  if (grid > (int64_t)num_sms * 8) grid = (int64_t)num_sms * 8;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = launch_pdl(widen_scales_kernel, dim3((unsigned)grid), dim3(256), 0, st,
+                             reinterpret_cast<const __half*>(Sw16), n, sw32);
+  if (e != cudaSuccess) return cuda_fail(e);
+  comet_status ls = check_launch();
+  if (ls != COMET_OK) return ls;
+  return gemm_common(Xq8, Xq4, Sx, ldsx, block_bits, M, K, Wq, sw32, N, group, Y, ldy, nullptr, workspace,
+                     (size_t)base, st);
+}
+
 int64_t comet_attention_kv4_workspace_bytes(int32_t T, int32_t H) {
   if (T <= 0 || H <= 0) return -1;
   return (int64_t)H * ((T + kAttChunk - 1) / kAttChunk) * kAttPart * 4;

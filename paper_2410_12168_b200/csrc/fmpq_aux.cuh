@@ -226,6 +226,59 @@ __global__ void __launch_bounds__(256) quantize_act_static_kernel(const __half* 
   if (o == 0) Sx[(int64_t)b * ldsx + m] = s;
 }
 
+// ---- f4: FP16 weight-scale storage ----------------
+// Per (row n, group of g permuted channels): a = max |w|, s = fp16_rn(fp32(a /
+// 7)) (a == 0 -> 1, a nonzero s that underflows -> 2^-24), q = clamp(rha(fp32(
+// w / s)), -7, 7) -- the scale the weights are quantized with is the stored
+// fp16 one.  Warp per (row, group) for g = 128 (lane = 4 channels), warp per
+// row for g = K; packed into the tiled layout like comet_pack_weight.
+template <bool kPerm>
+__global__ void __launch_bounds__(256) pack_weight_f16s_kernel(const __half* __restrict__ W, int64_t ldw, int N, int K,
+                                                               int group, const int32_t* __restrict__ perm,
+                                                               uint8_t* __restrict__ Wq, __half* __restrict__ Sw) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ng = K / group;
+  const int64_t item = (int64_t)blockIdx.x * 8 + warp;  // (row, group)
+  if (item >= (int64_t)N * ng) return;
+  const int64_t n = item / ng;
+  const int j = (int)(item % ng);
+  const unsigned short* row = reinterpret_cast<const unsigned short*>(W + n * ldw);
+  float a = 0.0f;
+  for (int i = lane; i < group; i += 32) {
+    const int c = j * group + i;
+    a = fmaxf(a, fabsf(half_bits_to_float(row[kPerm ? __ldg(perm + c) : c])));
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, off));
+  __half sh = __float2half_rn(1.0f);
+  if (a != 0.0f) {
+    sh = __float2half_rn(__fdiv_rn(a, 7.0f));
+    if (__half2float(sh) == 0.0f) sh = __ushort_as_half((unsigned short)1);  // 2^-24
+  }
+  const float sf = __half2float(sh);
+  // each lane packs whole 8-value words of the group: word w covers channels 8w .. 8w+7
+  for (int w = lane; w < group / 8; w += 32) {
+    int32_t q[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int c = j * group + 8 * w + e;
+      const float v = __fdiv_rn(half_bits_to_float(row[kPerm ? __ldg(perm + c) : c]), sf);
+      q[e] = fabsf(v) >= 8388608.0f ? (v > 0.0f ? 7 : -7) : min(7, max(-7, round_half_away(v)));
+    }
+    *reinterpret_cast<uint32_t*>(Wq + wq_tiled_offset(n, ((int64_t)j * group + 8 * w) / 2, K / 128)) =
+        pack_int4_word(q);
+  }
+  if (lane == 0) Sw[(int64_t)j * N + n] = sh;
+}
+
+// fp16 scales -> the fp32 scales the GEMM kernels read (per GEMM call, into the workspace)
+__global__ void __launch_bounds__(256) widen_scales_kernel(const __half* __restrict__ in, int64_t n,
+                                                           float* __restrict__ out) {
+  grid_dep_launch();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __half2float(in[i]);
+}
+
 // ---- f3: dequant-in-attention over the KV4 cache (§3.2, §6.1) ----
 // One decode query per head: o_h = softmax(scale * q_h . K^_h^T) V^_h with
 // K^, V^ = fp16_rn((q - zp) * s) of the KV4 cache (the dequantisation

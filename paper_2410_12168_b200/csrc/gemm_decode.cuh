@@ -35,9 +35,6 @@
 #include "quantize.cuh"
 #include "sm100.cuh"
 
-#ifndef COMET_DEC_EXP
-#define COMET_DEC_EXP 0  // timing experiments only: 1 = skip Sx loads, 2 = also skip X loads
-#endif
 
 namespace comet {
 
@@ -215,8 +212,7 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
   const uint32_t tmem_base = *tmem_holder;
 
 
-  if (COMET_DEC_EXP == 5) {
-  } else if (warp == 0) {
+  if (warp == 0) {
     // ------------------------------------------ a3: weight producer ----
     // only the HBM weight stream: one bulk copy per unit, nothing else on
     // this warp's issue path
@@ -261,11 +257,11 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
         uint32_t tx = 0;
 #pragma unroll
         for (int j = 0; j < C::kUB; ++j)
-          if (j < it.len && COMET_DEC_EXP < 2) tx += (map.code[it.b + j] >> 15) ? C::kBBytes : C::kXPBytes;
+          if (j < it.len) tx += (map.code[it.b + j] >> 15) ? C::kBBytes : C::kXPBytes;
         mbar_arrive_expect_tx(&xfull[s], tx);
 #pragma unroll
         for (int j = 0; j < C::kUB; ++j) {
-          if (j < it.len && COMET_DEC_EXP < 2) {
+          if (j < it.len) {
             const uint32_t code = map.code[it.b + j];
             const int rank = code & 0x7FFF;
             if (code >> 15)
@@ -283,10 +279,10 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
           uint8_t* slot = smem + C::kScaleBase + a * C::kSlotBytes;
           // sx of the unit's blocks: one [kUB x BN] box of Sx [nb x ldsx]
           // (columns >= ldsx and rows >= nb are zero-filled, still counted)
-          const uint32_t tx = (COMET_DEC_EXP >= 1 ? 0 : C::kSxBytes) +
+          const uint32_t tx = C::kSxBytes +
                               (kGroupK ? (seg_end ? 512 : 0) : C::kUB * 512);
           mbar_arrive_expect_tx(&sfull[a], tx);
-          if (COMET_DEC_EXP < 1) tma_load_2d(slot, &tmSx, &sfull[a], m0, it.b);
+          tma_load_2d(slot, &tmSx, &sfull[a], m0, it.b);
           if (!kGroupK)
             tma_load_2d(slot + C::kSxBytes, &tmSw, &sfull[a], n0, it.b);  // [kUB x 128] box of Sw [nb x N]
           else if (seg_end)
@@ -430,10 +426,6 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
       tc_fence_after();
       // one block's chunk of kChunk accumulator columns [c, c + kChunk)
       auto consume = [&](int jb, int c, const uint32_t* r) {
-        if (COMET_DEC_EXP == 3) {
-          y2[c / 2] += r[0];
-          return;
-        }
         const int b = it.b + jb;
         const bool is8 = (map.code[b] >> 15) != 0;
         if (kAccOut) {
@@ -457,8 +449,7 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
           }
         }
       };
-      if (COMET_DEC_EXP == 4) {
-      } else if constexpr (C::kCW <= 32) {
+      if constexpr (C::kCW <= 32) {
         // kLdG blocks' accumulators (<= 32 registers) in flight before one wait
 #pragma unroll
         for (int jb0 = 0; jb0 < C::kUB; jb0 += C::kLdG) {

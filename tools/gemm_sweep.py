@@ -157,13 +157,13 @@ def trace(M, N, K, n8, cta=0, units=24):
     L = comet.lib()
     L.comet_debug_cta_times.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
     L.comet_debug_trace.argtypes = [ctypes.c_void_p]
-    buf = (ctypes.c_ulonglong * 1280)()
+    buf = (ctypes.c_ulonglong * 2048)()
     L.comet_debug_trace(buf)  # clear-less: events of untraced units stay stale, print only < units
     L.comet_debug_cta_times(cta + 1, None, 0)
     run(M, N, K, n8, "K", reps=1)
     L.comet_debug_cta_times(0, None, 0)
     L.comet_debug_trace(buf)
-    a = np.array(buf[:], dtype=np.int64).reshape(20, 64)
+    a = np.array(buf[:], dtype=np.int64).reshape(32, 64)
     t0 = a[0, 0]
     names = ["Wiss", "Xiss", "arrive", "expd", "mma", "accrdy", "accrel", "retire", "epitop", "sxrdy"]
     print(f"M={M} N={N} K={K} CTA{cta} trace (cycles rel. first W issue):")
@@ -178,12 +178,12 @@ def trace3(M, N, K, n8, cta=0, steps=40):
     L = comet.lib()
     L.comet_debug_cta_times.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
     L.comet_debug_trace.argtypes = [ctypes.c_void_p]
-    buf = (ctypes.c_ulonglong * 1280)()
+    buf = (ctypes.c_ulonglong * 2048)()
     L.comet_debug_cta_times(cta + 1, None, 0)
     run(M, N, K, n8, "K", reps=1)
     L.comet_debug_cta_times(0, None, 0)
     L.comet_debug_trace(buf)
-    a = np.array(buf[:], dtype=np.int64).reshape(20, 64)
+    a = np.array(buf[:], dtype=np.int64).reshape(32, 64)
     t0 = a[0, 0]
     names = ["Ptop", "staged", "tfull0", "prom0", "-", "-", "mrdy", "mma0", "temty", "Wiss", "Xiss", "sxrdy"]
     print(f"M={M} N={N} K={K} CTA{cta} pf trace (cycles rel. first P iteration; staged = block g+2 staged):")
@@ -208,12 +208,12 @@ def trace2(M, N, K, n8, cta=0, steps=40):
     L = comet.lib()
     L.comet_debug_cta_times.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
     L.comet_debug_trace.argtypes = [ctypes.c_void_p]
-    buf = (ctypes.c_ulonglong * 1280)()
+    buf = (ctypes.c_ulonglong * 2048)()
     L.comet_debug_cta_times(cta + 1, None, 0)
     run(M, N, K, n8, "K", reps=1)
     L.comet_debug_cta_times(0, None, 0)
     L.comet_debug_trace(buf)
-    a = np.array(buf[:], dtype=np.int64).reshape(20, 64)
+    a = np.array(buf[:], dtype=np.int64).reshape(32, 64)
     t0 = a[0, 0]
     names = ["iter", "fullnx", "expdnx", "sxrdy", "accrdy", "promdn", "mma", "prod"]
     print(f"M={M} N={N} K={K} CTA{cta} prefill trace (cycles rel. first iteration; fullnx/expdnx = step g):")
