@@ -117,13 +117,19 @@ struct PfCfg {
 #endif
   static constexpr int kTileN = PF_TILEN;       // weight rows per pair tile (MMA N)
   static constexpr int kRows = kTileN / 2;      // weight rows per CTA
-  static constexpr int kPQ = kTileN / 64;       // promotion warps per TMEM lane quarter
+#ifndef PF_PQ
+#define PF_PQ (PF_TILEN / 64)
+#endif
+#ifndef PF_ACCS
+#define PF_ACCS 2
+#endif
+  static constexpr int kPQ = PF_PQ;             // promotion warps per TMEM lane quarter
   static constexpr int kPWarps = 4 * kPQ;       // 16 promotion warps
   static constexpr int kWCols = kTileN / kPQ;   // 64 accumulator columns per promotion warp
   static constexpr int kSWarps = PF_SWARPS;     // staging warps
   static constexpr int kStages = PF_STAGES;     // operand stages (A + B), freed by the MMA commit
   static constexpr int kLStages = PF_STAGES;    // packed weight stages, freed by the staging warps
-  static constexpr int kAccs = 2;               // kTileN-column accumulators
+  static constexpr int kAccs = PF_ACCS;         // kTileN-column accumulators
   static constexpr int kScaleSlots = 8;
   static constexpr int kABytes = 128 * 128;     // token rows x 128 B (SW128)
   static constexpr int kBBytes = kRows * 128;   // expanded weight rows x 128 B (SW128)
@@ -145,7 +151,7 @@ struct PfCfg {
   static_assert(kAccs * kTileN <= 512, "TMEM budget");
   static_assert(kWCols % 16 == 0, "x16 TMEM loads");
   static constexpr int kLoadWarp = 0, kMmaWarp = 1, kWLoadWarp = 2, kStageWarp = 3, kPBase = kStageWarp + kSWarps;
-  static_assert(kPBase + kPWarps <= 20, "20 warps keep 96 registers (warps are allocated in groups of four)");
+  // (warps get registers in groups of four: up to 20 warps keep 96 registers per thread)
   static constexpr int kThreads = 32 * (kPBase + kPWarps);
   static constexpr int kReadyCount = 2 * kSWarps;   // both CTAs' staging warps
   static constexpr int kTemptyCount = 2 * kPWarps;  // both CTAs' promotion warps
