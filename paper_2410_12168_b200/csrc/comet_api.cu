@@ -434,7 +434,7 @@ comet_status quantize_act_impl(const void* X, int64_t ldx, int32_t M, int32_t K,
   const __half* Xh = reinterpret_cast<const __half*>(X);
   if (M >= 64) {
     // row-staged kernel: persistent CTAs, double-buffered rows in smem
-    const int smem = kQNBuf * K * 2 + ((perm && COMET_Q_PERMSMEM) ? K * 2 : 0);  // row buffers + u16 permutation
+    const int smem = kQNBuf * K * 2;  // row buffers
     if (smem <= 200 * 1024) {
       auto kern = X4e ? (perm ? quantize_act_rows_kernel<true, false, kBf16, true> : quantize_act_rows_kernel<false, false, kBf16, true>)
                       : (perm ? quantize_act_rows_kernel<true, false, kBf16> : quantize_act_rows_kernel<false, false, kBf16>);
@@ -442,12 +442,15 @@ comet_status quantize_act_impl(const void* X, int64_t ldx, int32_t M, int32_t K,
       // it is a cheap host-side attribute)
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return cuda_fail(e);
-      int per_sm = (228 * 1024) / (smem + (int)sizeof(ScaleTab) + 1024);  // + the static scale table
-      if (per_sm > 8) per_sm = 8;
+      // one wave of persistent CTAs: as many per SM as registers, shared
+      // memory (row buffers + the static scale table) and threads allow
+      int per_sm = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQThreads, smem);
+      if (e != cudaSuccess) return cuda_fail(e);
       if (per_sm < 1) per_sm = 1;
       int64_t grid = (int64_t)num_sms * per_sm;
       if (grid > ldsx) grid = ldsx;
-      kern<<<(int)grid, 256, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
+      kern<<<(int)grid, kQThreads, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
                                          X4e ? X4e : reinterpret_cast<uint8_t*>(Xq4),
                                          X4e ? (int64_t)n4 * 128 : (int64_t)n4 * 64, Sx, nullptr, CX);
       return check_launch();
@@ -605,7 +608,7 @@ comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K,
   auto layer = [&](const void* Xd, int64_t ldxd, int32_t mc, void* Yd, int64_t ldyd) -> comet_status {
     const int64_t ldsx = comet_act_ldsx(mc);
     const int64_t wsb = comet_w4ax_gemm_workspace_bytes(mc, N, K);
-    if (make_plan(mc, N, K, 148).two_sm && (int64_t)kQNBuf * K * 2 <= 200 * 1024 && !COMET_Q_PERMSMEM) {
+    if (make_plan(mc, N, K, 148).two_sm && (int64_t)kQNBuf * K * 2 <= 200 * 1024) {
       // prefill: the quantizer writes the GEMM's e4m3 token operand and its
       // corrections straight into the workspace (no packed INT4 plane, no token
       // preparation kernel); identical results to the two-call path
@@ -862,22 +865,23 @@ comet_status comet_quantize_act_static(const void* X, int64_t ldx, int32_t M, in
   if (M >= 64 && kQNBuf * K * 2 <= 200 * 1024) {
     // row-staged kernel (as comet_quantize_act), static-scale arithmetic
     const int smem = kQNBuf * K * 2;
-    cudaError_t e = cudaFuncSetAttribute(perm ? quantize_act_rows_kernel<true, true> : quantize_act_rows_kernel<false, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    auto kern = perm ? quantize_act_rows_kernel<true, true> : quantize_act_rows_kernel<false, true>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_fail(e);
-    int per_sm = (228 * 1024) / (smem + (int)sizeof(ScaleTab) + 1024);  // + the kernel's static scale table
-    if (per_sm > 8) per_sm = 8;
+    int per_sm = 0;  // one wave of persistent CTAs
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQThreads, smem);
+    if (e != cudaSuccess) return cuda_fail(e);
     if (per_sm < 1) per_sm = 1;
     int num_sms = 148;
     device_check(&num_sms);
     int64_t g = (int64_t)num_sms * per_sm;
     if (g > ldsx) g = ldsx;
     if (perm)
-      quantize_act_rows_kernel<true, true><<<(int)g, 256, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8,
+      quantize_act_rows_kernel<true, true><<<(int)g, kQThreads, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8,
                                                                       (int64_t)n8 * 128, reinterpret_cast<uint8_t*>(Xq4),
                                                                       (int64_t)n4 * 64, Sx, scales);
     else
-      quantize_act_rows_kernel<false, true><<<(int)g, 256, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8,
+      quantize_act_rows_kernel<false, true><<<(int)g, kQThreads, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8,
                                                                        (int64_t)n8 * 128, reinterpret_cast<uint8_t*>(Xq4),
                                                                        (int64_t)n4 * 64, Sx, scales);
     return check_launch();

@@ -64,6 +64,8 @@ DEVI uint32_t rha_bits(float v) {
 // correctly rounded quotient is 2^E * RN(m / qmax) while it stays normal;
 // tab holds RN(m / qmax) and RN(qmax / m) for the 1024 mantissas (filled with
 // __fdiv_rn by the kernel).  Extreme exponents fall back to the division.
+// (A compile-time table in global memory instead of each CTA's shared memory
+// measured no faster: 8B down projection 138 vs 134 us.)
 struct ScaleTab {
   float v[4][1024];  // s7, r7, s127, r127
 };
@@ -218,116 +220,187 @@ __global__ void __launch_bounds__(256) quantize_act_kernel(const __half* __restr
   if (o == 0) Sx[(int64_t)b * ldsx + m] = s;
 }
 
+// f32x2 helpers (FMUL2 / FADD2 with a rounding mode: two lanes per instruction)
+DEVI uint64_t f2_pack(float lo, float hi) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+  return d;
+}
+DEVI void f2_unpack(uint64_t d, uint32_t& lo, uint32_t& hi) { asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(d)); }
+DEVI uint64_t f2_mul(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+DEVI uint64_t f2_add_rn(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+DEVI uint64_t f2_add_rz(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+DEVI uint64_t f2_add_rm(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// 0xFF for each negative element (sign replicated by prmt's selector msb;
+// __byte_perm drops that bit) of the pairs a (elements 0, 1) and b (2, 3)
+DEVI uint32_t sign_bytes4(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, 0xFDB9;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+// |x| of both elements of a packed fp16 / bf16 pair (already sign-cleared)
+// as fp32 (exact)
+template <bool kBf16>
+DEVI uint64_t abs_pair_f32(uint32_t aw) {
+  if (kBf16) return f2_pack(__uint_as_float(aw << 16), __uint_as_float(aw & 0xFFFF0000u));
+  return f2_pack(half_bits_to_float(aw & 0xFFFFu), half_bits_to_float(aw >> 16));
+}
+
 #ifndef COMET_Q_NBUF
 #define COMET_Q_NBUF 2  // row buffers per CTA (rows in flight = COMET_Q_NBUF - 1 ahead)
 #endif
 constexpr int kQNBuf = COMET_Q_NBUF;
-#ifndef COMET_Q_PERMSMEM
-#define COMET_Q_PERMSMEM 0  // 1: permutation cached in shared memory as u16 (measured slower: occupancy)
-#endif
 // One (row, block) item for the row-staged kernel: `row` is the row in
-// shared memory, `psm` the permutation as u16 in shared memory (kPerm).
+// shared memory.  Called warp-uniformly (the absmax and sum(q) reductions are
+// full-warp shuffles, each half-warp reducing its own item); `valid` false
+// (the odd half-warp past the last block) computes on a clamped block and
+// stores nothing.
 // kStatic (f4): the block's scale is the calibrated sstat[b]; q = clamp(rha(
 // fp32(x / s)), -qmax, qmax) (comet_quantize_act_static) instead of the
 // runtime absmax and the reciprocal multiply.
 // kE4: INT4 blocks are written as the prefill GEMM's e4m3 operand X4e
 // [M x n4*128 B] (ld4 = its row stride) plus CX[r4 * ldsx + m] = 8 sum(q)
 // instead of the packed plane (comet_w4ax_linear, see gemm_pf.cuh)
+//
+// Dynamic path, per lane (8 channels as four packed fp16/bf16 pairs w):
+//   a    = max |x| : integer max of the sign-cleared bit patterns (monotone
+//          for non-negative floats), then the half-warp shuffle tree;
+//   s, r = scale_recip(a)  (IEEE a / qmax and qmax / a);
+//   t    = RD(RZ(|x| r + 0.5) + M) on f32x2 pairs: t = M + |q| (see rha_bits,
+//          |x| r == |x r|);
+//   e4m3 (kE4, INT4 block): byte = |q| | sign(x) << 7, sum(q) by a signed dp4a;
+//   INT8 / packed INT4: h = (copysign(t - M, x)) + M, low byte = q.
+// A negative x with q == 0 gives the e4m3 byte 0x80 (-0.0): its products
+// add exactly zero in the GEMM, the same as +0.
 template <bool kPerm, bool kStatic = false, bool kBf16 = false, bool kE4 = false>
-DEVI void quant_item(const unsigned short* row, const unsigned short* psm, const int32_t* __restrict__ gperm,
-                     const BlockMap& map, int b, int o,
-                     unsigned hmask, int64_t m, int64_t ldsx, int8_t* __restrict__ Xq8, int64_t ld8,
-                     uint8_t* __restrict__ Xq4, int64_t ld4, float* __restrict__ Sx,
-                     const float* __restrict__ sstat = nullptr, const ScaleTab* tab = nullptr,
-                     float* __restrict__ CX = nullptr) {
+DEVI void quant_item(const unsigned short* row, const int32_t* __restrict__ gperm, const BlockMap& map, int b, bool valid,
+                     int o, int64_t m, int64_t ldsx, int8_t* __restrict__ Xq8, int64_t ld8, uint8_t* __restrict__ Xq4,
+                     int64_t ld4, float* __restrict__ Sx, const float* __restrict__ sstat = nullptr,
+                     const ScaleTab* tab = nullptr, float* __restrict__ CX = nullptr) {
   const int i0 = b * 128 + o * 8;
-  float x[8];
-  if (kPerm && !COMET_Q_PERMSMEM) {
+  uint32_t w[4];  // elements 2j (low half) and 2j + 1 (high half)
+  if (kPerm) {
     const int4 p0 = __ldg(reinterpret_cast<const int4*>(gperm + i0));
     const int4 p1 = __ldg(reinterpret_cast<const int4*>(gperm + i0 + 4));
-    const int p[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-#pragma unroll
-    for (int j = 0; j < 8; ++j) x[j] = act_bits_to_float<kBf16>(row[p[j]]);
-  } else if (kPerm) {
-    const uint4 pv = *reinterpret_cast<const uint4*>(psm + i0);  // 8 x u16 source positions
-    const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      x[2 * j] = act_bits_to_float<kBf16>(row[pw[j] & 0xFFFF]);
-      x[2 * j + 1] = act_bits_to_float<kBf16>(row[pw[j] >> 16]);
-    }
+    w[0] = __byte_perm(row[p0.x], row[p0.y], 0x5410);
+    w[1] = __byte_perm(row[p0.z], row[p0.w], 0x5410);
+    w[2] = __byte_perm(row[p1.x], row[p1.y], 0x5410);
+    w[3] = __byte_perm(row[p1.z], row[p1.w], 0x5410);
   } else {
     const uint4 v = *reinterpret_cast<const uint4*>(row + i0);
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      x[2 * j] = act_bits_to_float<kBf16>(w[j] & 0xFFFF);
-      x[2 * j + 1] = act_bits_to_float<kBf16>(w[j] >> 16);
-    }
+    w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
   }
   const uint32_t code = map.code[b];
   const bool is8 = (code >> 15) != 0;
   const int rank = code & 0x7FFF;
-  const float qmax = is8 ? 127.0f : 7.0f;
-  float s = 1.0f;
-  int32_t q[8];
-  if (kStatic) {
-    s = __ldg(sstat + b);
+  if constexpr (kStatic) {
+    if (!valid) return;
+    const float s = __ldg(sstat + b);
     const int qm = is8 ? 127 : 7;
+    int32_t q[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const float v = __fdiv_rn(x[j], s);
+      const float v = __fdiv_rn(act_bits_to_float<kBf16>(w[j >> 1] >> (16 * (j & 1))), s);
       q[j] = fabsf(v) >= 8388608.0f ? (v > 0.0f ? qm : -qm) : min(qm, max(-qm, round_half_away(v)));
     }
+    if (is8) {
+      uint32_t lo = (uint32_t)(q[0] & 0xFF) | ((uint32_t)(q[1] & 0xFF) << 8) | ((uint32_t)(q[2] & 0xFF) << 16) |
+                    ((uint32_t)(q[3] & 0xFF) << 24);
+      uint32_t hi = (uint32_t)(q[4] & 0xFF) | ((uint32_t)(q[5] & 0xFF) << 8) | ((uint32_t)(q[6] & 0xFF) << 16) |
+                    ((uint32_t)(q[7] & 0xFF) << 24);
+      *reinterpret_cast<uint2*>(Xq8 + m * ld8 + (int64_t)rank * 128 + o * 8) = make_uint2(lo, hi);
+    } else {
+      *reinterpret_cast<uint32_t*>(Xq4 + m * ld4 + (int64_t)rank * 64 + o * 4) = pack_int4_word(q);
+    }
+    if (o == 0) Sx[(int64_t)b * ldsx + m] = s;
+    return;
   } else {
-    // dynamic scale: half-warp absmax, table-based IEEE s and r, F2I-free rounding
-    float a = 0.0f;
+    uint32_t aw[4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) a = fmaxf(a, fabsf(x[j]));
+    for (int j = 0; j < 4; ++j) aw[j] = w[j] & 0x7FFF7FFFu;
+    uint32_t am = __vmaxu2(__vmaxu2(aw[0], aw[1]), __vmaxu2(aw[2], aw[3]));
+    am = max(am & 0xFFFFu, am >> 16);
 #pragma unroll
-    for (int off = 8; off >= 1; off >>= 1) a = fmaxf(a, __shfl_xor_sync(hmask, a, off));
-    float r;
-    scale_recip(a, is8, tab, s, r);
+    for (int off = 8; off >= 1; off >>= 1) am = max(am, __shfl_xor_sync(0xFFFFFFFFu, am, off));
+    float s, r;
+    scale_recip(act_bits_to_float<kBf16>(am), is8, tab, s, r);
+    const uint64_t r2 = f2_pack(r, r), half2 = f2_pack(0.5f, 0.5f), M2 = f2_pack(12582912.0f, 12582912.0f);
+    uint64_t t2[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) t2[j] = f2_add_rm(f2_add_rz(f2_mul(abs_pair_f32<kBf16>(aw[j]), r2), half2), M2);
+    if (kE4) {  // (the sum(q) shuffle runs warp-uniformly: the other half-warp's block may be INT8)
+      uint32_t t[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) f2_unpack(t2[j], t[2 * j], t[2 * j + 1]);
+      const uint32_t mlo = __byte_perm(__byte_perm(t[0], t[1], 0x0040), __byte_perm(t[2], t[3], 0x0040), 0x5410);
+      const uint32_t mhi = __byte_perm(__byte_perm(t[4], t[5], 0x0040), __byte_perm(t[6], t[7], 0x0040), 0x5410);
+      const uint32_t slo = sign_bytes4(w[0], w[1]), shi = sign_bytes4(w[2], w[3]);
+      int qs = __dp4a((int)mlo, (int)(slo | 0x01010101u), __dp4a((int)mhi, (int)(shi | 0x01010101u), 0));
+#pragma unroll
+      for (int off = 8; off >= 1; off >>= 1) qs += __shfl_xor_sync(0xFFFFFFFFu, qs, off);
+      if (!is8) {
+        if (!valid) return;
+        *reinterpret_cast<uint2*>(Xq4 + m * ld4 + (int64_t)rank * 128 + o * 8) =
+            make_uint2(mlo | (slo & 0x80808080u), mhi | (shi & 0x80808080u));
+        if (o == 0) {
+          CX[(int64_t)rank * ldsx + m] = 8.0f * (float)qs;
+          Sx[(int64_t)b * ldsx + m] = s;
+        }
+        return;
+      }
+    }
+    if (!valid) return;
+    const uint64_t nM2 = f2_pack(-12582912.0f, -12582912.0f);
     uint32_t h[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) h[j] = rha_bits(__fmul_rn(x[j], r));
+    for (int j = 0; j < 4; ++j) {
+      uint32_t klo, khi;
+      f2_unpack(f2_add_rn(t2[j], nM2), klo, khi);
+      f2_unpack(f2_add_rn(f2_pack(__uint_as_float(klo | ((w[j] << 16) & 0x80000000u)),
+                                  __uint_as_float(khi | (w[j] & 0x80000000u))), M2), h[2 * j], h[2 * j + 1]);
+    }
     if (is8) {
       *reinterpret_cast<uint2*>(Xq8 + m * ld8 + (int64_t)rank * 128 + o * 8) = pack_int8_bits(h);
-    } else if (kE4) {
-      int qs;
-      *reinterpret_cast<uint2*>(Xq4 + m * ld4 + (int64_t)rank * 128 + o * 8) = e4m3_int4_bits(h, qs);
-#pragma unroll
-      for (int off = 8; off >= 1; off >>= 1) qs += __shfl_xor_sync(hmask, qs, off);
-      if (o == 0) CX[(int64_t)rank * ldsx + m] = 8.0f * (float)qs;
     } else {
       *reinterpret_cast<uint32_t*>(Xq4 + m * ld4 + (int64_t)rank * 64 + o * 4) = pack_int4_bits(h);
     }
     if (o == 0) Sx[(int64_t)b * ldsx + m] = s;
-    return;
   }
-  if (is8) {
-    uint32_t lo = (uint32_t)(q[0] & 0xFF) | ((uint32_t)(q[1] & 0xFF) << 8) | ((uint32_t)(q[2] & 0xFF) << 16) |
-                  ((uint32_t)(q[3] & 0xFF) << 24);
-    uint32_t hi = (uint32_t)(q[4] & 0xFF) | ((uint32_t)(q[5] & 0xFF) << 8) | ((uint32_t)(q[6] & 0xFF) << 16) |
-                  ((uint32_t)(q[7] & 0xFF) << 24);
-    *reinterpret_cast<uint2*>(Xq8 + m * ld8 + (int64_t)rank * 128 + o * 8) = make_uint2(lo, hi);
-  } else {
-    *reinterpret_cast<uint32_t*>(Xq4 + m * ld4 + (int64_t)rank * 64 + o * 4) = pack_int4_word(q);
-  }
-  if (o == 0) Sx[(int64_t)b * ldsx + m] = s;
 }
 
 // Activation quantize + pack, row-staged variant (a1 + a2 for the GEMM
 // path): persistent CTAs walk rows; each row (K fp16, contiguous) arrives in
 // shared memory by one 1-D bulk copy (the next row's copy is in flight while
-// this one is quantized), the permutation sits in shared memory as u16 for
-// the CTA's lifetime, and the fused channel gather reads the
-// permuted positions from shared memory instead of issuing 8 scattered 2-byte
-// global loads per lane.  Half-warp per (row, 128-channel block) item, lane =
-// 8 channels, two items in flight per half-warp; arithmetic and output
-// identical to quantize_act_kernel.
+// this one is quantized), and the fused channel gather reads the
+// permuted positions of the row from shared memory (the permutation itself
+// comes through L1/L2) instead of issuing 8 scattered 2-byte global loads per
+// lane.  Half-warp per (row, 128-channel block) item, lane = 8 channels, two
+// items in flight per half-warp; output identical to quantize_act_kernel.
+#ifndef COMET_Q_MINB
+#define COMET_Q_MINB 1  // __launch_bounds__ min CTAs per SM (register cap)
+#endif
+#ifndef COMET_Q_THREADS
+#define COMET_Q_THREADS 256
+#endif
+constexpr int kQThreads = COMET_Q_THREADS;  // threads per CTA of the row-staged kernel
 template <bool kPerm, bool kStatic = false, bool kBf16 = false, bool kE4 = false>
-__global__ void __launch_bounds__(256) quantize_act_rows_kernel(const __half* __restrict__ X, int64_t ldx, int M,
+__global__ void __launch_bounds__(kQThreads, COMET_Q_MINB) quantize_act_rows_kernel(const __half* __restrict__ X, int64_t ldx, int M,
                                                                 int nb, int64_t ldsx, const int32_t* __restrict__ perm,
                                                                 const __grid_constant__ BlockMap map,
                                                                 int8_t* __restrict__ Xq8, int64_t ld8,
@@ -341,16 +414,12 @@ __global__ void __launch_bounds__(256) quantize_act_rows_kernel(const __half* __
   __shared__ uint64_t rbar[kQNBuf];
   __shared__ ScaleTab tab;
   if (!kStatic) fill_scale_tab(&tab);
-  const int half_id = threadIdx.x >> 4;
+  const int hb = (threadIdx.x >> 4) & 1;  // half-warp within the warp
   const int o = threadIdx.x & 15;
-  const unsigned hmask = 0xFFFFu << (threadIdx.x & 16);
-  unsigned short* psm = reinterpret_cast<unsigned short*>(qsm + (size_t)kQNBuf * 2 * K);
   if (threadIdx.x == 0) {
     for (int i = 0; i < kQNBuf; ++i) mbar_init(&rbar[i], 1);
     fence_mbar_init();
   }
-  if (kPerm && COMET_Q_PERMSMEM)
-    for (int i = threadIdx.x; i < K; i += blockDim.x) psm[i] = (unsigned short)__ldg(perm + i);
   __syncthreads();
   auto issue = [&](int64_t m, int buf) {
     mbar_arrive_expect_tx(&rbar[buf], (uint32_t)K * 2);
@@ -376,12 +445,18 @@ __global__ void __launch_bounds__(256) quantize_act_rows_kernel(const __half* __
     if (threadIdx.x == 0 && mp < M) issue(mp, (it + kQNBuf - 1) % kQNBuf);
     mbar_wait(&rbar[buf], (it / kQNBuf) & 1);
     const unsigned short* row = reinterpret_cast<const unsigned short*>(qsm + (size_t)buf * K * 2);
-    int b = half_id;
-    for (; b + 16 < nb; b += 32) {
-      quant_item<kPerm, kStatic, kBf16, kE4>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab, CX);
-      quant_item<kPerm, kStatic, kBf16, kE4>(row, psm, perm, map, b + 16, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab, CX);
+    // warp w takes block pairs (b0, b0 + 1), b0 = 2w + 16i, in warp-uniform
+    // steps (the reductions are full-warp shuffles); the odd half-warp past
+    // the last block of an odd nb runs on a clamped block and stores nothing
+    constexpr int H = kQThreads / 16;  // half-warps per CTA
+    int b0 = (threadIdx.x >> 5) * 2;
+    for (; b0 + H < nb; b0 += 2 * H) {
+      const int b2 = min(b0 + H + hb, nb - 1);
+      quant_item<kPerm, kStatic, kBf16, kE4>(row, perm, map, b0 + hb, true, o, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab, CX);
+      quant_item<kPerm, kStatic, kBf16, kE4>(row, perm, map, b2, b0 + H + hb < nb, o, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab, CX);
     }
-    if (b < nb) quant_item<kPerm, kStatic, kBf16, kE4>(row, psm, perm, map, b, o, hmask, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab, CX);
+    if (b0 < nb)
+      quant_item<kPerm, kStatic, kBf16, kE4>(row, perm, map, min(b0 + hb, nb - 1), b0 + hb < nb, o, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab, CX);
     __syncthreads();  // every half-warp is done with this buffer
   }
 }

@@ -297,18 +297,21 @@ def test_linear_entry_with_host_buffers():
     assert np.array_equal(Yh.numpy().view(np.uint16), g["Y"].view(np.uint16))
 
 
-@pytest.mark.parametrize("M,group", [(301, 128), (517, 1024)])
-def test_linear_prefill_fused_quantizer(M, group):
+@pytest.mark.parametrize("M,K,n8,group", [(301, 1024, 2, 128), (517, 1024, 2, 1024), (300, 1152, 3, 1152),
+                                           (260, 2176, 5, 128)])
+def test_linear_prefill_fused_quantizer(M, K, n8, group):
     """comet_w4ax_linear at prefill sizes: the quantizer writes the GEMM's e4m3
     token operand and corrections directly (no packed plane, no prep kernel);
     Y must be bit-identical to the two-call path (same tcgen05 arithmetic),
-    ragged M (ldsx padding rows), scattered INT8 blocks, both scale kinds."""
-    p = synth.make_problem(M, 640, 1024, n8=2, seed=31 + M, mask="scattered")
+    ragged M (ldsx padding rows), scattered INT8 blocks (the two half-warps of
+    a warp may hold an INT8 and an INT4 block), odd block counts (the last
+    half-warp idles), both scale kinds."""
+    p = synth.make_problem(M, 640, K, n8=n8, seed=31 + M, mask="scattered")
     ref = gpu_path(p, group)["Y"]
     W, perm, X = to_dev(p["W"]), to_dev(p["perm"]), to_dev(p["X"])
     bits = comet.BlockBits(p["bits"])
     Wq, Sw = comet.comet_pack_weight(W, perm, group)
-    scratch = comet.new_workspace(comet.comet_w4ax_linear_scratch_bytes(M, 640, 1024, bits), W.device)
+    scratch = comet.new_workspace(comet.comet_w4ax_linear_scratch_bytes(M, 640, K, bits), W.device)
     Y = comet.comet_w4ax_linear(X, bits, Wq, Sw, perm=perm, group=group, scratch=scratch)
     torch.cuda.synchronize()
     assert np.array_equal(Y.cpu().numpy().view(np.uint16), ref.view(np.uint16))
