@@ -266,11 +266,12 @@ DEVI uint64_t abs_pair_f32(uint32_t aw) {
 #define COMET_Q_NBUF 2  // row buffers per CTA (rows in flight = COMET_Q_NBUF - 1 ahead)
 #endif
 constexpr int kQNBuf = COMET_Q_NBUF;
-// One (row, block) item for the row-staged kernel: `row` is the row in
+// One (row, block) item for the row-staged kernel: 128 / kL lanes, each
+// holding kL consecutive channels of the permuted axis; `row` is the row in
 // shared memory.  Called warp-uniformly (the absmax and sum(q) reductions are
-// full-warp shuffles, each half-warp reducing its own item); `valid` false
-// (the odd half-warp past the last block) computes on a clamped block and
-// stores nothing.
+// full-warp shuffles, each lane group reducing its own item); `valid` false
+// (a lane group past the last block) computes on a clamped block and stores
+// nothing.
 // kStatic (f4): the block's scale is the calibrated sstat[b]; q = clamp(rha(
 // fp32(x / s)), -qmax, qmax) (comet_quantize_act_static) instead of the
 // runtime absmax and the reciprocal multiply.
@@ -278,9 +279,9 @@ constexpr int kQNBuf = COMET_Q_NBUF;
 // [M x n4*128 B] (ld4 = its row stride) plus CX[r4 * ldsx + m] = 8 sum(q)
 // instead of the packed plane (comet_w4ax_linear, see gemm_pf.cuh)
 //
-// Dynamic path, per lane (8 channels as four packed fp16/bf16 pairs w):
+// Dynamic path, per lane (kL channels as kL/2 packed fp16/bf16 pairs w):
 //   a    = max |x| : integer max of the sign-cleared bit patterns (monotone
-//          for non-negative floats), then the half-warp shuffle tree;
+//          for non-negative floats), then the lane-group shuffle tree;
 //   s, r = scale_recip(a)  (IEEE a / qmax and qmax / a);
 //   t    = RD(RZ(|x| r + 0.5) + M) on f32x2 pairs: t = M + |q| (see rha_bits,
 //          |x| r == |x r|);
@@ -288,23 +289,29 @@ constexpr int kQNBuf = COMET_Q_NBUF;
 //   INT8 / packed INT4: h = (copysign(t - M, x)) + M, low byte = q.
 // A negative x with q == 0 gives the e4m3 byte 0x80 (-0.0): its products
 // add exactly zero in the GEMM, the same as +0.
-template <bool kPerm, bool kStatic = false, bool kBf16 = false, bool kE4 = false>
+template <int kL, bool kPerm, bool kStatic = false, bool kBf16 = false, bool kE4 = false>
 DEVI void quant_item(const unsigned short* row, const int32_t* __restrict__ gperm, const BlockMap& map, int b, bool valid,
                      int o, int64_t m, int64_t ldsx, int8_t* __restrict__ Xq8, int64_t ld8, uint8_t* __restrict__ Xq4,
                      int64_t ld4, float* __restrict__ Sx, const float* __restrict__ sstat = nullptr,
                      const ScaleTab* tab = nullptr, float* __restrict__ CX = nullptr) {
-  const int i0 = b * 128 + o * 8;
-  uint32_t w[4];  // elements 2j (low half) and 2j + 1 (high half)
+  static_assert(kL == 8 || kL == 16, "8 or 16 channels per lane");
+  constexpr int kW = kL / 2;             // packed pairs per lane
+  constexpr int kLanes = 128 / kL;       // lanes per item
+  const int i0 = b * 128 + o * kL;
+  uint32_t w[kW];  // elements 2j (low half) and 2j + 1 (high half)
   if (kPerm) {
-    const int4 p0 = __ldg(reinterpret_cast<const int4*>(gperm + i0));
-    const int4 p1 = __ldg(reinterpret_cast<const int4*>(gperm + i0 + 4));
-    w[0] = __byte_perm(row[p0.x], row[p0.y], 0x5410);
-    w[1] = __byte_perm(row[p0.z], row[p0.w], 0x5410);
-    w[2] = __byte_perm(row[p1.x], row[p1.y], 0x5410);
-    w[3] = __byte_perm(row[p1.z], row[p1.w], 0x5410);
+#pragma unroll
+    for (int v = 0; v < kL / 4; ++v) {
+      const int4 p = __ldg(reinterpret_cast<const int4*>(gperm + i0) + v);
+      w[2 * v] = __byte_perm(row[p.x], row[p.y], 0x5410);
+      w[2 * v + 1] = __byte_perm(row[p.z], row[p.w], 0x5410);
+    }
   } else {
-    const uint4 v = *reinterpret_cast<const uint4*>(row + i0);
-    w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+#pragma unroll
+    for (int v = 0; v < kL / 8; ++v) {
+      const uint4 u = *reinterpret_cast<const uint4*>(row + i0 + 8 * v);
+      w[4 * v] = u.x, w[4 * v + 1] = u.y, w[4 * v + 2] = u.z, w[4 * v + 3] = u.w;
+    }
   }
   const uint32_t code = map.code[b];
   const bool is8 = (code >> 15) != 0;
@@ -313,51 +320,64 @@ DEVI void quant_item(const unsigned short* row, const int32_t* __restrict__ gper
     if (!valid) return;
     const float s = __ldg(sstat + b);
     const int qm = is8 ? 127 : 7;
-    int32_t q[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float v = __fdiv_rn(act_bits_to_float<kBf16>(w[j >> 1] >> (16 * (j & 1))), s);
-      q[j] = fabsf(v) >= 8388608.0f ? (v > 0.0f ? qm : -qm) : min(qm, max(-qm, round_half_away(v)));
-    }
-    if (is8) {
-      uint32_t lo = (uint32_t)(q[0] & 0xFF) | ((uint32_t)(q[1] & 0xFF) << 8) | ((uint32_t)(q[2] & 0xFF) << 16) |
-                    ((uint32_t)(q[3] & 0xFF) << 24);
-      uint32_t hi = (uint32_t)(q[4] & 0xFF) | ((uint32_t)(q[5] & 0xFF) << 8) | ((uint32_t)(q[6] & 0xFF) << 16) |
-                    ((uint32_t)(q[7] & 0xFF) << 24);
-      *reinterpret_cast<uint2*>(Xq8 + m * ld8 + (int64_t)rank * 128 + o * 8) = make_uint2(lo, hi);
-    } else {
-      *reinterpret_cast<uint32_t*>(Xq4 + m * ld4 + (int64_t)rank * 64 + o * 4) = pack_int4_word(q);
+    for (int g = 0; g < kL / 8; ++g) {
+      int32_t q[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float v = __fdiv_rn(act_bits_to_float<kBf16>(w[4 * g + (j >> 1)] >> (16 * (j & 1))), s);
+        q[j] = fabsf(v) >= 8388608.0f ? (v > 0.0f ? qm : -qm) : min(qm, max(-qm, round_half_away(v)));
+      }
+      if (is8) {
+        uint32_t lo = (uint32_t)(q[0] & 0xFF) | ((uint32_t)(q[1] & 0xFF) << 8) | ((uint32_t)(q[2] & 0xFF) << 16) |
+                      ((uint32_t)(q[3] & 0xFF) << 24);
+        uint32_t hi = (uint32_t)(q[4] & 0xFF) | ((uint32_t)(q[5] & 0xFF) << 8) | ((uint32_t)(q[6] & 0xFF) << 16) |
+                      ((uint32_t)(q[7] & 0xFF) << 24);
+        *reinterpret_cast<uint2*>(Xq8 + m * ld8 + (int64_t)rank * 128 + o * kL + 8 * g) = make_uint2(lo, hi);
+      } else {
+        *reinterpret_cast<uint32_t*>(Xq4 + m * ld4 + (int64_t)rank * 64 + o * (kL / 2) + 4 * g) = pack_int4_word(q);
+      }
     }
     if (o == 0) Sx[(int64_t)b * ldsx + m] = s;
     return;
   } else {
-    uint32_t aw[4];
+    uint32_t aw[kW];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) aw[j] = w[j] & 0x7FFF7FFFu;
-    uint32_t am = __vmaxu2(__vmaxu2(aw[0], aw[1]), __vmaxu2(aw[2], aw[3]));
+    for (int j = 0; j < kW; ++j) aw[j] = w[j] & 0x7FFF7FFFu;
+    uint32_t am = aw[0];
+#pragma unroll
+    for (int j = 1; j < kW; ++j) am = __vmaxu2(am, aw[j]);
     am = max(am & 0xFFFFu, am >> 16);
 #pragma unroll
-    for (int off = 8; off >= 1; off >>= 1) am = max(am, __shfl_xor_sync(0xFFFFFFFFu, am, off));
+    for (int off = kLanes / 2; off >= 1; off >>= 1) am = max(am, __shfl_xor_sync(0xFFFFFFFFu, am, off));
     float s, r;
     scale_recip(act_bits_to_float<kBf16>(am), is8, tab, s, r);
     const uint64_t r2 = f2_pack(r, r), half2 = f2_pack(0.5f, 0.5f), M2 = f2_pack(12582912.0f, 12582912.0f);
-    uint64_t t2[4];
+    uint64_t t2[kW];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) t2[j] = f2_add_rm(f2_add_rz(f2_mul(abs_pair_f32<kBf16>(aw[j]), r2), half2), M2);
-    if (kE4) {  // (the sum(q) shuffle runs warp-uniformly: the other half-warp's block may be INT8)
-      uint32_t t[8];
+    for (int j = 0; j < kW; ++j) t2[j] = f2_add_rm(f2_add_rz(f2_mul(abs_pair_f32<kBf16>(aw[j]), r2), half2), M2);
+    if (kE4) {  // (the sum(q) shuffle runs warp-uniformly: another lane group's block may be INT8)
+      uint32_t e[kL / 4];
+      int qs = 0;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) f2_unpack(t2[j], t[2 * j], t[2 * j + 1]);
-      const uint32_t mlo = __byte_perm(__byte_perm(t[0], t[1], 0x0040), __byte_perm(t[2], t[3], 0x0040), 0x5410);
-      const uint32_t mhi = __byte_perm(__byte_perm(t[4], t[5], 0x0040), __byte_perm(t[6], t[7], 0x0040), 0x5410);
-      const uint32_t slo = sign_bytes4(w[0], w[1]), shi = sign_bytes4(w[2], w[3]);
-      int qs = __dp4a((int)mlo, (int)(slo | 0x01010101u), __dp4a((int)mhi, (int)(shi | 0x01010101u), 0));
+      for (int g = 0; g < kL / 4; ++g) {  // 4 channels per e4m3 word
+        uint32_t t0, t1, t2w, t3;
+        f2_unpack(t2[2 * g], t0, t1);
+        f2_unpack(t2[2 * g + 1], t2w, t3);
+        const uint32_t mag = __byte_perm(__byte_perm(t0, t1, 0x0040), __byte_perm(t2w, t3, 0x0040), 0x5410);
+        const uint32_t sg = sign_bytes4(w[2 * g], w[2 * g + 1]);
+        qs = __dp4a((int)mag, (int)(sg | 0x01010101u), qs);
+        e[g] = mag | (sg & 0x80808080u);
+      }
 #pragma unroll
-      for (int off = 8; off >= 1; off >>= 1) qs += __shfl_xor_sync(0xFFFFFFFFu, qs, off);
+      for (int off = kLanes / 2; off >= 1; off >>= 1) qs += __shfl_xor_sync(0xFFFFFFFFu, qs, off);
       if (!is8) {
         if (!valid) return;
-        *reinterpret_cast<uint2*>(Xq4 + m * ld4 + (int64_t)rank * 128 + o * 8) =
-            make_uint2(mlo | (slo & 0x80808080u), mhi | (shi & 0x80808080u));
+        uint8_t* dst = Xq4 + m * ld4 + (int64_t)rank * 128 + o * kL;
+        if constexpr (kL == 16)
+          *reinterpret_cast<uint4*>(dst) = make_uint4(e[0], e[1], e[2], e[3]);
+        else
+          *reinterpret_cast<uint2*>(dst) = make_uint2(e[0], e[1]);
         if (o == 0) {
           CX[(int64_t)rank * ldsx + m] = 8.0f * (float)qs;
           Sx[(int64_t)b * ldsx + m] = s;
@@ -367,18 +387,21 @@ DEVI void quant_item(const unsigned short* row, const int32_t* __restrict__ gper
     }
     if (!valid) return;
     const uint64_t nM2 = f2_pack(-12582912.0f, -12582912.0f);
-    uint32_t h[8];
+    uint32_t h[kL];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < kW; ++j) {
       uint32_t klo, khi;
       f2_unpack(f2_add_rn(t2[j], nM2), klo, khi);
       f2_unpack(f2_add_rn(f2_pack(__uint_as_float(klo | ((w[j] << 16) & 0x80000000u)),
                                   __uint_as_float(khi | (w[j] & 0x80000000u))), M2), h[2 * j], h[2 * j + 1]);
     }
-    if (is8) {
-      *reinterpret_cast<uint2*>(Xq8 + m * ld8 + (int64_t)rank * 128 + o * 8) = pack_int8_bits(h);
-    } else {
-      *reinterpret_cast<uint32_t*>(Xq4 + m * ld4 + (int64_t)rank * 64 + o * 4) = pack_int4_bits(h);
+#pragma unroll
+    for (int g = 0; g < kL / 8; ++g) {
+      const uint32_t(&h8)[8] = *reinterpret_cast<const uint32_t(*)[8]>(h + 8 * g);
+      if (is8)
+        *reinterpret_cast<uint2*>(Xq8 + m * ld8 + (int64_t)rank * 128 + o * kL + 8 * g) = pack_int8_bits(h8);
+      else
+        *reinterpret_cast<uint32_t*>(Xq4 + m * ld4 + (int64_t)rank * 64 + o * (kL / 2) + 4 * g) = pack_int4_bits(h8);
     }
     if (o == 0) Sx[(int64_t)b * ldsx + m] = s;
   }
@@ -414,8 +437,17 @@ __global__ void __launch_bounds__(kQThreads, COMET_Q_MINB) quantize_act_rows_ker
   __shared__ uint64_t rbar[kQNBuf];
   __shared__ ScaleTab tab;
   if (!kStatic) fill_scale_tab(&tab);
-  const int hb = (threadIdx.x >> 4) & 1;  // half-warp within the warp
-  const int o = threadIdx.x & 15;
+  // channels per lane: 16 for a contiguous row (two 16-byte smem loads per
+  // lane); 8 with the permutation, whose gather is per element: with 16 the
+  // lanes of a warp read positions 16 apart, which for the mostly monotone
+  // FMPQ permutation (outliers first, the rest in order) piles 8-16
+  // lanes onto the same banks (8192 x 4096: 51 vs 45 us; without the
+  // permutation 31 vs 35 us)
+  constexpr int kL = kPerm ? 8 : 16;
+  constexpr int kLanes = 128 / kL;         // lanes per (row, block) item
+  constexpr int kS = kQThreads / kLanes;   // items per CTA pass
+  const int sub = (threadIdx.x & 31) / kLanes;  // item slot within the warp
+  const int o = threadIdx.x % kLanes;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kQNBuf; ++i) mbar_init(&rbar[i], 1);
     fence_mbar_init();
@@ -445,19 +477,20 @@ __global__ void __launch_bounds__(kQThreads, COMET_Q_MINB) quantize_act_rows_ker
     if (threadIdx.x == 0 && mp < M) issue(mp, (it + kQNBuf - 1) % kQNBuf);
     mbar_wait(&rbar[buf], (it / kQNBuf) & 1);
     const unsigned short* row = reinterpret_cast<const unsigned short*>(qsm + (size_t)buf * K * 2);
-    // warp w takes block pairs (b0, b0 + 1), b0 = 2w + 16i, in warp-uniform
-    // steps (the reductions are full-warp shuffles); the odd half-warp past
-    // the last block of an odd nb runs on a clamped block and stores nothing
-    constexpr int H = kQThreads / 16;  // half-warps per CTA
-    int b0 = (threadIdx.x >> 5) * 2;
-    for (; b0 + H < nb; b0 += 2 * H) {
-      const int b2 = min(b0 + H + hb, nb - 1);
-      quant_item<kPerm, kStatic, kBf16, kE4>(row, perm, map, b0 + hb, true, o, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab, CX);
-      quant_item<kPerm, kStatic, kBf16, kE4>(row, perm, map, b2, b0 + H + hb < nb, o, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab, CX);
+    // warp w takes blocks b0 .. b0 + 32/kLanes - 1, b0 = (32/kLanes) w + kS i,
+    // in warp-uniform steps (the reductions are full-warp shuffles); a lane
+    // group past the last block runs on a clamped block and stores nothing
+    int b0 = (threadIdx.x >> 5) * (32 / kLanes);
+    for (; b0 + kS < nb; b0 += 2 * kS) {
+      quant_item<kL, kPerm, kStatic, kBf16, kE4>(row, perm, map, b0 + sub, true, o, m, ldsx, Xq8, ld8, Xq4, ld4, Sx,
+                                                 sstat, &tab, CX);
+      quant_item<kL, kPerm, kStatic, kBf16, kE4>(row, perm, map, min(b0 + kS + sub, nb - 1), b0 + kS + sub < nb, o, m,
+                                                 ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab, CX);
     }
     if (b0 < nb)
-      quant_item<kPerm, kStatic, kBf16, kE4>(row, perm, map, min(b0 + hb, nb - 1), b0 + hb < nb, o, m, ldsx, Xq8, ld8, Xq4, ld4, Sx, sstat, &tab, CX);
-    __syncthreads();  // every half-warp is done with this buffer
+      quant_item<kL, kPerm, kStatic, kBf16, kE4>(row, perm, map, min(b0 + sub, nb - 1), b0 + sub < nb, o, m, ldsx, Xq8,
+                                                 ld8, Xq4, ld4, Sx, sstat, &tab, CX);
+    __syncthreads();  // every lane group is done with this buffer
   }
 }
 
