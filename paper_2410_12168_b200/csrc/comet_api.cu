@@ -25,6 +25,9 @@ namespace {
 
 thread_local char g_cuda_err[256] = "";
 std::atomic<int64_t> g_launches{0};
+// tools only (comet_debug_set_pf_clusters): CTA pairs of the prefill grid,
+// 0 = one persistent pair per SM pair (the product schedule)
+std::atomic<int> g_pf_clusters{0};
 
 comet_status cuda_fail(cudaError_t e) {
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
@@ -206,8 +209,8 @@ Plan make_plan(int M, int N, int K, int num_sms) {
 }
 
 template <bool kGroupK, bool kAcc>
-comet_status launch_gemm_pf(const CUtensorMap& tmXe, const CUtensorMap& tmX8, const BlockMap& map,
-                            const GemmArgs& args, const Plan& p, cudaStream_t st) {
+comet_status launch_gemm_pf(const CUtensorMap& tmXe, const CUtensorMap& tmX8, const CUtensorMap& tmY,
+                            const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
   using C = PfCfg;
   auto kern = w4ax_gemm_pf_kernel<kGroupK, kAcc>;
   static AttrCache cache;
@@ -216,11 +219,12 @@ comet_status launch_gemm_pf(const CUtensorMap& tmXe, const CUtensorMap& tmX8, co
   PfSched sched;
   sched.m_tiles = p.m_tiles;
   sched.tiles = p.m_tiles * p.n_tiles;
-  sched.clusters = sched.tiles < p.clusters ? sched.tiles : p.clusters;
+  const int want = g_pf_clusters.load(std::memory_order_relaxed) > 0 ? g_pf_clusters.load() : p.clusters;
+  sched.clusters = sched.tiles < want ? sched.tiles : want;
   // PDL: the prologue (barrier init, TMEM allocation) overlaps the token
   // preparation kernel; the producers wait for it before their first load
-  cudaError_t e = launch_pdl(kern, dim3(2 * sched.clusters), dim3(C::kThreads), C::kSmemBytes, st, tmXe, tmX8, map,
-                             args, sched);
+  cudaError_t e = launch_pdl(kern, dim3(2 * sched.clusters), dim3(C::kThreads), C::kSmemBytes, st, tmXe, tmX8, tmY,
+                             map, args, sched);
   if (e != cudaSuccess) return cuda_fail(e);
   return check_launch();
 }
@@ -276,12 +280,12 @@ comet_status launch_decode_bn(const CUtensorMap& tmX4, const CUtensorMap& tmX8, 
 }
 
 template <bool kAcc>
-comet_status launch_gemm(const CUtensorMap& tmXp, const CUtensorMap& tmX8, const BlockMap& map,
-                         const GemmArgs& args, const Plan& p, cudaStream_t st) {
+comet_status launch_gemm(const CUtensorMap& tmXp, const CUtensorMap& tmX8, const CUtensorMap& tmY,
+                         const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
   const bool group_k = args.group_blocks == args.nb;
   if (p.two_sm) {
-    if (group_k) return launch_gemm_pf<true, kAcc>(tmXp, tmX8, map, args, p, st);
-    return launch_gemm_pf<false, kAcc>(tmXp, tmX8, map, args, p, st);
+    if (group_k) return launch_gemm_pf<true, kAcc>(tmXp, tmX8, tmY, map, args, p, st);
+    return launch_gemm_pf<false, kAcc>(tmXp, tmX8, tmY, map, args, p, st);
   }
   if (group_k) return launch_decode_bn<true, kAcc>(tmXp, tmX8, map, args, p, st);
   return launch_decode_bn<false, kAcc>(tmXp, tmX8, map, args, p, st);
@@ -338,6 +342,14 @@ comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, in
   }
   if (!n8) tmX8 = tmXp;  // never dereferenced
   if (!n4) tmXp = tmX8;
+  // a8 (prefill): Y [M x N] fp16 as bytes, box 32 rows x 64 B (one promotion
+  // warp's 32 rows x 32 columns), SW64 so the row-per-lane smem writes are
+  // conflict-free; out-of-range rows / columns of a tile are clipped by TMA
+  CUtensorMap tmY = tmX8;
+  if (p.two_sm && !Acc) {
+    if (!make_map_u8(&tmY, Y, (uint64_t)N * 2, (uint64_t)M, (uint64_t)ldy * 2, 64, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+      return map_fail("Y");
+  }
   GemmArgs a;
   a.M = M;
   a.N = N;
@@ -366,8 +378,8 @@ comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, in
     comet_status ls = check_launch();
     if (ls != COMET_OK) return ls;
   }
-  if (Acc) return launch_gemm<true>(tmXp, tmX8, map, a, p, st);
-  return launch_gemm<false>(tmXp, tmX8, map, a, p, st);
+  if (Acc) return launch_gemm<true>(tmXp, tmX8, tmY, map, a, p, st);
+  return launch_gemm<false>(tmXp, tmX8, tmY, map, a, p, st);
 }
 
 // comet_w4ax_linear with host buffers: two internal copy streams and their
@@ -971,5 +983,13 @@ int comet_debug_trace(unsigned long long* host2048) {  // 32 x 64 entries
   return cudaMemcpyFromSymbol(host2048, g_trace, sizeof(unsigned long long) * 2048) == cudaSuccess ? 0 : -1;
 }
 int64_t comet_launch_count(void) { return g_launches.load(); }
+// Schedule ablation (tools/a7_ablation.py): the prefill kernel's grid as n CTA
+// pairs (n > 74: more pairs than SM pairs, each taking one tile, the
+// hardware scheduling them in waves -- the paper's non-persistent "static"
+// schedule); 0 restores the persistent grid.  Results are identical.
+int comet_debug_set_pf_clusters(int n) {
+  g_pf_clusters.store(n < 0 ? 0 : n);
+  return 0;
+}
 
 }  // extern "C"

@@ -113,7 +113,7 @@ struct PfCfg {
 #define PF_SWARPS 4
 #endif
 #ifndef PF_STAGES
-#define PF_STAGES 5
+#define PF_STAGES 4
 #endif
   static constexpr int kTileN = PF_TILEN;       // weight rows per pair tile (MMA N)
   static constexpr int kRows = kTileN / 2;      // weight rows per CTA
@@ -144,7 +144,11 @@ struct PfCfg {
   static constexpr int kBarBase = kScaleBase + kScaleSlots * kSlotBytes;
   static constexpr int kBarBytes = 512;
   static constexpr int kFacBase = kBarBase + kBarBytes;       // float fac[nb]
-  static constexpr int kSmemBytes = kFacBase + 512 * 4 + 1024;
+  // a8: per promotion warp one 32-row x 32-column fp16 box (2 KB, SW64) for
+  // the TMA store of Y
+  static constexpr int kYWarpBytes = 32 * 64;
+  static constexpr int kYBase = (kFacBase + 512 * 4 + 1023) / 1024 * 1024;
+  static constexpr int kSmemBytes = kYBase + kPWarps * kYWarpBytes + 1024;
   static_assert(kABase % 1024 == 0 && kBBase % 1024 == 0 && kBBytes % 1024 == 0, "SW128 operand alignment");
   static_assert(kWPBase % 128 == 0 && kScaleBase % 16 == 0, "alignment");
   static_assert(kSmemBytes <= 227 * 1024, "smem budget");
@@ -213,7 +217,8 @@ __global__ void __launch_bounds__(256) prep_tokens_kernel(const uint8_t* __restr
 template <bool kGroupK, bool kAccOut>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
     w4ax_gemm_pf_kernel(const __grid_constant__ CUtensorMap tmXe, const __grid_constant__ CUtensorMap tmX8,
-                        const __grid_constant__ BlockMap map, GemmArgs args, PfSched sched) {
+                        const __grid_constant__ CUtensorMap tmY, const __grid_constant__ BlockMap map, GemmArgs args,
+                        PfSched sched) {
   using C = PfCfg;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
@@ -261,6 +266,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
   if (warp == C::kLoadWarp && lane == 0) {
     tma_prefetch_desc(&tmXe);
     tma_prefetch_desc(&tmX8);
+    tma_prefetch_desc(&tmY);
   }
   if (warp == C::kMmaWarp) tmem_alloc_2sm<512>(tmem_holder);
   tc_fence_before();
@@ -530,38 +536,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
       }
 
       if (++b == nb) {
-        // -------------------- a8: tile write-back (fp16 RNE, direct stores) ----
+        // -------------------- a8: tile write-back (fp16 RNE, TMA stores) -------
+        // y = sw * (z - zc) (per-channel) -> fp16 RNE -> the warp's 2 KB box
+        // in shared memory (row = lane, SW64 chunks: conflict-free) -> one
+        // TMA store per 32 columns.  (Direct 16-byte stores from the
+        // row-per-lane layout touch 32 rows per instruction; their burst at
+        // every tile end stalled the staging warps' smem stores and the
+        // promotion for ~3 us per tile.)
         if (!kAccOut) {
           int m0, n0;
           sched.coords(t, m0, n0);
-          const int m = m0 + 128 * (int)crank + row;
-          const int nu = n0 + kWC * kw;
           const uint64_t nzc2 = pack2(-zc, -zc);
           const uint32_t swa = slot + C::kSwOff + (kWC * kw) * 4;
-          __half* yrow = args.Y + (int64_t)m * args.ldy + nu;
-          // 8 columns at a time: two per-channel scale quads, four fp16 pairs, one 16-byte store
-          // (a tile may straddle N: N % 128 == 0, tiles are 256 wide)
+          const uint32_t ybuf = sbase + C::kYBase + (warp - C::kPBase) * C::kYWarpBytes;
 #pragma unroll
-          for (int v = 0; v < kWC / 8; ++v) {
-            uint32_t hw[4];
+          for (int h = 0; h < kWC / 32; ++h) {
+            if (lane == 0) bulk_wait_group_read0();  // the previous box has left the buffer
+            __syncwarp();
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int p4 = 2 * v + h;
-              uint64_t v0 = y[2 * p4], v1 = y[2 * p4 + 1];
-              if (kGroupK) {  // per-channel weight scales, once per tile
-                const float4 w4 = lds_f32x4(swa + 16 * p4);
-                v0 = mul2_u(add2_u(v0, nzc2), pack2(w4.x, w4.y));
-                v1 = mul2_u(add2_u(v1, nzc2), pack2(w4.z, w4.w));
+            for (int v4 = 0; v4 < 4; ++v4) {  // 8 columns: one 16-byte chunk of the row
+              const int v = 4 * h + v4;
+              uint32_t hw[4];
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                const int p4 = 2 * v + hh;
+                uint64_t v0 = y[2 * p4], v1 = y[2 * p4 + 1];
+                if (kGroupK) {  // per-channel weight scales, once per tile
+                  const float4 w4 = lds_f32x4(swa + 16 * p4);
+                  v0 = mul2_u(add2_u(v0, nzc2), pack2(w4.x, w4.y));
+                  v1 = mul2_u(add2_u(v1, nzc2), pack2(w4.z, w4.w));
+                }
+                __half2 h0 = __float22half2_rn(unpack2(v0));
+                __half2 h1 = __float22half2_rn(unpack2(v1));
+                hw[2 * hh] = *reinterpret_cast<uint32_t*>(&h0);
+                hw[2 * hh + 1] = *reinterpret_cast<uint32_t*>(&h1);
+                y[2 * p4] = 0;
+                y[2 * p4 + 1] = 0;
               }
-              __half2 h0 = __float22half2_rn(unpack2(v0));
-              __half2 h1 = __float22half2_rn(unpack2(v1));
-              hw[2 * h] = *reinterpret_cast<uint32_t*>(&h0);
-              hw[2 * h + 1] = *reinterpret_cast<uint32_t*>(&h1);
-              y[2 * p4] = 0;
-              y[2 * p4 + 1] = 0;
+              sts128(ybuf + lane * 64 + ((v4 ^ ((lane >> 1) & 3)) << 4), make_uint4(hw[0], hw[1], hw[2], hw[3]));
             }
-            if (m < args.M && nu + 8 * v < args.N)
-              *reinterpret_cast<uint4*>(yrow + 8 * v) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmY, ybuf, 2 * (n0 + kWC * kw + 32 * h), m0 + 128 * (int)crank + 32 * q);
+              bulk_commit_group();
+            }
           }
           zc = 0.f;
         }
@@ -574,6 +593,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
     }
   }
 
+  if (warp >= C::kPBase && lane == 0) bulk_wait_group0();  // Y stores complete before the CTA exits
   tc_fence_before();
   __syncthreads();
   cluster_sync();
