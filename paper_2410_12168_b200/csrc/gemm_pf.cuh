@@ -144,9 +144,13 @@ struct PfCfg {
   static constexpr int kBarBase = kScaleBase + kScaleSlots * kSlotBytes;
   static constexpr int kBarBytes = 512;
   static constexpr int kFacBase = kBarBase + kBarBytes;       // float fac[nb]
-  // a8: per promotion warp one 32-row x 32-column fp16 box (2 KB, SW64) for
-  // the TMA store of Y
-  static constexpr int kYWarpBytes = 32 * 64;
+  // a8: per promotion warp kYBoxes 32-row x 32-column fp16 boxes (2 KB each,
+  // SW64) for the TMA stores of Y
+#ifndef PF_YBOXES
+#define PF_YBOXES 2
+#endif
+  static constexpr int kYBoxes = PF_YBOXES;
+  static constexpr int kYWarpBytes = kYBoxes * 32 * 64;
   static constexpr int kYBase = (kFacBase + 512 * 4 + 1023) / 1024 * 1024;
   static constexpr int kSmemBytes = kYBase + kPWarps * kYWarpBytes + 1024;
   static_assert(kABase % 1024 == 0 && kBBase % 1024 == 0 && kBBytes % 1024 == 0, "SW128 operand alignment");
@@ -551,8 +555,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
           const uint32_t ybuf = sbase + C::kYBase + (warp - C::kPBase) * C::kYWarpBytes;
 #pragma unroll
           for (int h = 0; h < kWC / 32; ++h) {
-            if (lane == 0) bulk_wait_group_read0();  // the previous box has left the buffer
-            __syncwarp();
+            const uint32_t ybox = ybuf + (h % C::kYBoxes) * 2048;
+            if (h % C::kYBoxes == 0) {  // the previous boxes have left the buffer
+              if (lane == 0) bulk_wait_group_read0();
+              __syncwarp();
+            }
 #pragma unroll
             for (int v4 = 0; v4 < 4; ++v4) {  // 8 columns: one 16-byte chunk of the row
               const int v = 4 * h + v4;
@@ -573,12 +580,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
                 y[2 * p4] = 0;
                 y[2 * p4 + 1] = 0;
               }
-              sts128(ybuf + lane * 64 + ((v4 ^ ((lane >> 1) & 3)) << 4), make_uint4(hw[0], hw[1], hw[2], hw[3]));
+              sts128(ybox + lane * 64 + ((v4 ^ ((lane >> 1) & 3)) << 4), make_uint4(hw[0], hw[1], hw[2], hw[3]));
             }
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&tmY, ybuf, 2 * (n0 + kWC * kw + 32 * h), m0 + 128 * (int)crank + 32 * q);
+              tma_store_2d(&tmY, ybox, 2 * (n0 + kWC * kw + 32 * h), m0 + 128 * (int)crank + 32 * q);
               bulk_commit_group();
             }
           }
