@@ -970,6 +970,10 @@ comet_status comet_dequantize_kv(const void* Q, const float* scale, const uint8_
 int comet_debug_cta_times(int enable, unsigned long long* host, int n) {
   int on = enable;
   if (cudaMemcpyToSymbol(g_cta_times_on, &on, sizeof(int)) != cudaSuccess) return -1;
+  if (on) {  // fresh event table for the traced run
+    static const unsigned long long zeros[32 * 64] = {};
+    if (cudaMemcpyToSymbol(g_trace, zeros, sizeof(zeros)) != cudaSuccess) return -1;
+  }
   if (host && n > 0) {
     if (n > 1024) n = 1024;
     if (cudaMemcpyFromSymbol(host, g_cta_times, sizeof(unsigned long long) * 3 * n) != cudaSuccess) return -1;

@@ -87,6 +87,10 @@ __device__ unsigned long long g_trace[32][64];
 DEVI void trace(bool on, int ev, int i) {
   if (kTraceBuild && on && i < 64) g_trace[ev][i] = clk64();
 }
+// per-warp clocks of one step: g_trace[row][slot]
+DEVI void trace_at(bool on, int row, int slot) {
+  if (kTraceBuild && on) g_trace[row][slot] = clk64();
+}
 DEVI uint32_t smid() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));

@@ -1,43 +1,39 @@
 // gemm_pf.cuh -- prefill W4Ax GEMM (M > 128 tokens) on CTA pairs
-// (tcgen05 cta_group::2), persistent over pair tiles of 256 tokens x 256
+// (tcgen05 cta_group::2), persistent over pair tiles of 256 tokens x 192
 // weight rows, K walked one 128-channel FMPQ block at a time.
 //
-// Per block, one MMA item of 4 x K=32 tcgen05.mma (M=256, N=256) into one of
-// two 256-column TMEM accumulators (all 512 columns), so the promotion of
-// block b overlaps the MMAs of block b+1 (the paper's overlap of conversion
-// and MMA):
+// Per block, one MMA item of 4 x K=32 tcgen05.mma (M=256, N=192) into one of
+// two 192-column TMEM accumulators, so the promotion of block b overlaps the
+// MMAs of block b+1 (the paper's overlap of conversion and MMA):
 //   INT4 block (W4A4): kind::f8f6f4, e4m3 x e4m3 -> fp32.  Tokens are
-//       q * 2^-9 (exact e4m3 subnormals, converted once per call by
-//       prep_tokens_kernel), weights (q + 8) * 2^-9 (the nibble XOR 8: e4m3
-//       bytes 0..15 are exactly u * 2^-9).  Every product is an exact
-//       multiple of 2^-18 and the tensor core's fp32 sum of them is exact
-//       (|sum| < 2^15 * 2^-18; tools/microbench_fp8.cu checks it against the
-//       integer sum), so the accumulator holds D = 2^-18 (acc + 8 sum xq) with
-//       acc the INT32 block sum of O6, already in fp32: the promotion needs no
-//       int -> float conversion.
+//       q * 2^-9 (exact e4m3 subnormals, written by the quantizer in
+//       comet_w4ax_linear or by prep_tokens_kernel), weights (q + 8) * 2^-9
+//       (the nibble XOR 8: e4m3 bytes 0..15 are exactly u * 2^-9).  Every
+//       product is an exact multiple of 2^-18 and the tensor core's fp32 sum
+//       of them is exact (|sum| < 2^15 * 2^-18; tools/microbench_fp8.cu checks
+//       it against the integer sum), so the accumulator holds
+//       D = 2^-18 (acc + 8 sum xq) with acc the INT32 block sum of O6, already
+//       in fp32: the promotion needs no int -> float conversion.
 //   INT8 block (W4A8): kind::i8, xq x 16*wq -> int32 (the zero extension
 //       "multiplied by 16"), promoted with cvt.rn.f32.s32.
 // A (tokens) and B (weights) are shared-memory operands (SS MMA): A is a TMA
 // box of the CTA's 128 token rows x 128 B (SW128; the INT8 plane or the e4m3
-// token plane), B the CTA's 128 packed weight rows expanded by the staging
-// warps into a SW128 K-major stage.  The 256-wide tile keeps the L2 -> SM
-// stream at ~26 KB per block per SM (51 B/clk at the MMA rate; the e4m3 token
-// rows are 62% of it), the two accumulators cover the ~500-cycle MMA
-// round trip, and 16 promotion warps hold the 128 x 256 fp32 running sums in
-// registers (64 per thread).
+// token plane), B the CTA's 96 packed weight rows expanded by the staging
+// warps into a SW128 K-major stage.
 //
-// Roles per CTA (20 warps = 640 threads, 96 registers; registers are
-// allocated for warps in groups of four, so a 21st warp would cost 80):
-//   warp 0  (a3) token + scale producer: TMA of the token block, bulk copies
+// Roles per CTA (19 warps = 608 threads, 96 registers; registers are
+// allocated to warps in groups of four, so a 21st warp would cost 80):
+//   warps 0-11  (a6, a8) promotion: thread = token row (TMEM lane), 64
+//           columns read with double-buffered tcgen05.ld x8, the accumulator
+//           released after its last load; running sums in registers; at the
+//           tile's last block fp16 RNE -> a 32 x 32 smem box per warp -> TMA
+//           tensor store
+//   warp 12 (a3) token + scale producer: TMA of the token block, bulk copies
 //           of Sx, the e4m3 correction 8*sum(xq) and the weight scales
-//   warp 1  (a5) MMA issuer (leader CTA only), commits to both CTAs
-//   warp 2  (a3) weight producer: 1-D bulk copies of the tiled packed rows
-//   warps 3-6   (a4) staging: packed weight chunks -> e4m3 (INT4 block) or
+//   warp 13 (a5) MMA issuer (leader CTA only), commits to both CTAs
+//   warp 14 (a3) weight producer: 1-D bulk copies of the tiled packed rows
+//   warps 15-18 (a4) staging: packed weight chunks -> e4m3 (INT4 block) or
 //           INT8 x16 (INT8 block) in the SW128 B stage
-//   warps 4-19  (a6, a8) promotion: thread = token row (TMEM lane), 64
-//           columns read with four tcgen05.ld x16, the accumulator released
-//           before the last chunk's math; at the tile's last block fp16 RNE ->
-//           direct global stores
 #pragma once
 #include <cuda_fp16.h>
 #include <stdint.h>
@@ -158,9 +154,15 @@ struct PfCfg {
   static_assert(kSmemBytes <= 227 * 1024, "smem budget");
   static_assert(kAccs * kTileN <= 512, "TMEM budget");
   static_assert(kWCols % 16 == 0, "x16 TMEM loads");
-  static constexpr int kLoadWarp = 0, kMmaWarp = 1, kWLoadWarp = 2, kStageWarp = 3, kPBase = kStageWarp + kSWarps;
+  // Warp ids: promotion warps first (the warp schedulers favour low ids and
+  // the promotion is the critical path), then the token producer, MMA issuer,
+  // weight producer and staging warps.  Measured against producers-first
+  // (0 load, 1 MMA, 2 weights, 3-6 staging, 7-18 promotion): 70B gate_up
+  // 4041 -> 3906 us; MMA warp first (0 MMA, 1-12 promotion) 3919-3930 us.
+  static constexpr int kPBase = 0, kLoadWarp = kPWarps, kMmaWarp = kPWarps + 1, kWLoadWarp = kPWarps + 2,
+                       kStageWarp = kPWarps + 3;
   // (warps get registers in groups of four: up to 20 warps keep 96 registers per thread)
-  static constexpr int kThreads = 32 * (kPBase + kPWarps);
+  static constexpr int kThreads = 32 * (3 + kSWarps + kPWarps);  // producers + MMA, staging, promotion
   static constexpr int kReadyCount = 2 * kSWarps;   // both CTAs' staging warps
   static constexpr int kTemptyCount = 2 * kPWarps;  // both CTAs' promotion warps
 };
@@ -386,7 +388,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
         if (pt < sched.tiles) sched.coords(pt, pm0, pn0);
       }
     }
-  } else if (warp >= C::kStageWarp && warp < C::kPBase) {
+  } else if (warp >= C::kStageWarp && warp < C::kStageWarp + C::kSWarps) {
     // ------------- a4 staging: packed weight chunks -> SW128 B operand ----
     const int et = (int)threadIdx.x - 32 * C::kStageWarp;  // 0 .. 32 kSWarps - 1
     const uint32_t leader_ready = mapa_shared(smem_u32(ready), 0);
@@ -441,8 +443,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
       trace(tr_s, 11, j);
 
     }
-  } else if (warp >= C::kPBase) {
-    // ------------------------- warps 4-19: a6 promotion + a8 write-back ----
+  } else if (warp >= C::kPBase && warp < C::kPBase + C::kPWarps) {
+    // ------------------------- warps 0-11: a6 promotion + a8 write-back ----
     const int q = warp & 3;                  // TMEM lane quarter
     const int kw = (warp - C::kPBase) >> 2;  // columns [64 kw, 64 kw + 64) of the tile
     const int row = 32 * q + lane;           // token row within this CTA
@@ -467,6 +469,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
       trace(tr_p && ev0 == 0, 0, g);
       mbar_wait(&tfull[acc], (g / C::kAccs) & 1);
       trace(tr_p, ev0 + 1, g);
+      // steps 16..19: every promotion warp's "accumulator seen" / "released" clocks
+      trace_at(tr && lane == 0 && g >= 16 && g < 20, 25 + (g - 16), 2 * (warp - C::kPBase));
       tc_fence_after();
       const uint32_t ta = tl + acc * C::kTileN;
       float sxv = 0.f, cxv = 0.f;
@@ -534,6 +538,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(leader_tempty + acc * 8);
           trace(tr_p, ev0 + 2, g);
+          trace_at(tr && lane == 0 && g >= 16 && g < 20, 25 + (g - 16), 2 * (warp - C::kPBase) + 1);
         }
         promote8(c + 1, rb);
         if (c + 2 < kC8) tmem_ld_wait_dep(ra);
@@ -600,7 +605,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
     }
   }
 
-  if (warp >= C::kPBase && lane == 0) bulk_wait_group0();  // Y stores complete before the CTA exits
+  if (warp >= C::kPBase && warp < C::kPBase + C::kPWarps && lane == 0) bulk_wait_group0();  // Y stores complete before the CTA exits
   tc_fence_before();
   __syncthreads();
   cluster_sync();

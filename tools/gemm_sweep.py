@@ -246,6 +246,14 @@ def trace_pf(M, N, K, n8, cta=0, steps=64, group="K"):
     print("MMA issue detail: temty, elected, after MMA0, after MMA3, after commit0, after commit1; then P19 tfull/release")
     for i in range(8, 24):
         print(f"  {i:3d} " + " ".join(f"{a[e, i] - t0:7d}" for e in (6, 16, 17, 18, 19, 7, 15)))
+    print("accumulator hand-off, steps 16..19, CTA0's 12 promotion warps: seen / released (rel. the step's commit)")
+    for i in range(16, 20):
+        r = a[25 + i - 16]
+        seen = [int(r[2 * w] - a[7, i]) for w in range(12)]
+        rel = [int(r[2 * w + 1] - a[7, i]) for w in range(12)]
+        print(f"  {i:3d} commit {a[7, i] - t0:7d}  MMA sees free (step+2) +{a[6, i + 2] - a[7, i]}")
+        print("       seen " + " ".join(f"{x:5d}" for x in seen))
+        print("       rel  " + " ".join(f"{x:5d}" for x in rel))
     print("staging detail: mdone seen, LDS landed, weights stored, tokens st issued, proxy fence done, st wait done, ready arrived")
     for i in range(8, 24):
         print(f"  {i:3d} " + " ".join(f"{a[e, i] - t0:7d}" for e in (10, 20, 21, 22, 23, 24, 11)))
