@@ -82,8 +82,9 @@ struct DecCfg {
   // expansion groups of 4 warps (one per TMEM lane quarter) take alternate
   // units, so two units' LDS -> zero-extend -> tcgen05.st chains overlap
   static constexpr int kExpGroups = BN >= 128 ? 1 : 2;
-  static constexpr int kEpiWarp0 = 4 + 4 * kExpGroups;
-  static constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
+  // warp ids (epilogue warps first measured the same: 70B gate_up M=16 59.4 us)
+  static constexpr int kWWarp = 0, kMmaWarp = 1, kXWarp = 2, kExpWarp0 = 4, kEpiWarp0 = 4 + 4 * kExpGroups;
+  static constexpr int kThreads = 32 * (4 + 4 * kExpGroups + kEpiWarps);
   static constexpr int kSmemNeed = kBarBase + 1024 + 1024;
   // > half of the SM's 228 KB: exactly one CTA per SM (stream-K divides the
   // work by CTA, and each CTA owns all 512 TMEM columns)
@@ -199,20 +200,20 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
     for (int a = 0; a < C::kASlots; ++a) mbar_init(&aempty[a], 1);
     fence_mbar_init();
   }
-  if (warp == 2 && lane == 0) {
+  if (warp == C::kXWarp && lane == 0) {
     tma_prefetch_desc(&tmX4);
     tma_prefetch_desc(&tmX8);
     tma_prefetch_desc(&tmSx);
     if (!kGroupK) tma_prefetch_desc(&tmSw);
   }
-  if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_holder);
+  if (warp == C::kMmaWarp) tmem_alloc<C::kTmemCols>(tmem_holder);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
 
-  if (warp == 0) {
+  if (warp == C::kWWarp) {
     // ------------------------------------------ a3: weight producer ----
     // only the HBM weight stream: one bulk copy per unit, nothing else on
     // this warp's issue path
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
       __syncwarp();
     }
     rt.flush(0);
-  } else if (warp == 2) {
+  } else if (warp == C::kXWarp) {
     // ---------------------------------- a3: token + scale producer ----
     grid_dep_wait();  // PDL: the planes and scales come from the preceding quantizer
     const bool tr_on = g_cta_times_on && blockIdx.x + 1 == g_cta_times_on && lane == 0;
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
       }
       __syncwarp();
     }
-  } else if (warp == 1) {
+  } else if (warp == C::kMmaWarp) {
     // ------------------------------------------------------ a5: MMA ----
     constexpr uint32_t idesc = idesc_i8(128, BN);
     RoleTimer rt(g_cta_times_on && blockIdx.x + 1 == g_cta_times_on && lane == 0);
@@ -324,13 +325,13 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
       __syncwarp();
     }
     rt.flush(1);
-  } else if (warp >= 4 && warp < C::kEpiWarp0) {
+  } else if (warp >= C::kExpWarp0 && warp < C::kExpWarp0 + 4 * C::kExpGroups) {
     // ------------------------------------------ a4: expansion warps ----
     const int q = warp & 3;
     const int row = 32 * q + lane;  // weight row of the tile = TMEM lane
-    const int grp = (warp - 4) >> 2;
-    const int tid = threadIdx.x - 128 - 128 * grp;
-    RoleTimer rt(g_cta_times_on && blockIdx.x + 1 == g_cta_times_on && warp == 4 && lane == 0);
+    const int grp = (warp - C::kExpWarp0) >> 2;
+    const int tid = threadIdx.x - 32 * C::kExpWarp0 - 128 * grp;
+    RoleTimer rt(g_cta_times_on && blockIdx.x + 1 == g_cta_times_on && warp == C::kExpWarp0 && lane == 0);
     int i = 0;
     for (It it(u0, u1, nb, sched.n_tiles); it.valid(); it.next(nb), ++i) {
       if (C::kExpGroups > 1 && (i % C::kExpGroups) != grp) continue;
@@ -397,7 +398,7 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
       trace(rt.on, 3, i);
     }
     rt.flush(2);
-  } else if (warp >= C::kEpiWarp0) {
+  } else if (warp >= C::kEpiWarp0 && warp < C::kEpiWarp0 + C::kEpiWarps) {
     // ----------------------------------------- a6-a8: epilogue warps ----
     const int q = warp & 3;
     const int h = (warp - C::kEpiWarp0) >> 2;  // column group
@@ -585,7 +586,7 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc<C::kTmemCols>(tmem_base);
+  if (warp == C::kMmaWarp) tmem_dealloc<C::kTmemCols>(tmem_base);
   if (threadIdx.x == 0 && g_cta_times_on && blockIdx.x < 1024) g_cta_times[3 * blockIdx.x + 1] = global_ns();
 }
 
