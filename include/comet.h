@@ -160,8 +160,14 @@ comet_status comet_w4ax_gemm_acc_i32(const int8_t* Xq8, const void* Xq4, const f
  * ordered after the caller's earlier work on `stream` (X: M*K*2 bytes in,
  * Y: M*N*2 bytes out); later work on `stream` is ordered after the copies.
  * scratch: device memory of at least comet_w4ax_linear_scratch_bytes(M, N,
- * K, block_bits) bytes, first 64 KiB zero on first use.  When Y is a host
- * pointer the call synchronizes `stream` before returning. */
+ * K, block_bits) bytes, first 64 KiB zero on first use.  The call does not
+ * synchronize: with host buffers, X must stay unchanged and Y unread until
+ * `stream` has been synchronized (as for cudaMemcpyAsync).  The input copies
+ * of a host-buffer call that directly follows another host-buffer call on the
+ * same stream start once that call's compute is done (not its output
+ * copies, unless this call's staged X overlaps the scratch bytes they read),
+ * so consecutive layers overlap H2D and D2H; work enqueued on `stream`
+ * between two such calls must not write either call's scratch. */
 comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
                                const uint8_t* block_bits, const void* Wq, const float* Sw, int32_t N, int32_t group,
                                void* Y, int64_t ldy, void* scratch, size_t scratch_bytes, comet_stream_t stream);

@@ -390,8 +390,12 @@ def comet_w4ax_gemm_acc_i32(Xq8, Xq4, Sx, bits, Wq, Sw, group: int = BLOCK, work
 
 
 def comet_w4ax_linear(X: torch.Tensor, bits, Wq, Sw, perm=None, group: int = BLOCK, out: Optional[torch.Tensor] = None,
-                      scratch: Optional[torch.Tensor] = None, stream=None):
-    """Whole linear layer through the C ABI; X / out may be host (pinned) tensors."""
+                      scratch: Optional[torch.Tensor] = None, stream=None, sync: bool = True):
+    """Whole linear layer through the C ABI; X / out may be host (pinned) tensors.
+    The C call only enqueues the work; with a host `out` and sync=True this
+    synchronizes the stream so `out` is complete on return (sync=False: the
+    caller synchronizes, and consecutive host-buffer calls overlap their
+    copies)."""
     b = as_bits(bits)
     M, K = X.shape
     N = Wq.shape[0]
@@ -402,6 +406,8 @@ def comet_w4ax_linear(X: torch.Tensor, bits, Wq, Sw, perm=None, group: int = BLO
     st = lib().comet_w4ax_linear(_ptr(X), X.stride(0), M, K, _ptr(perm), b.ptr, _ptr(Wq), _ptr(Sw), N, group,
                                  _ptr(Y), Y.stride(0), _ptr(scratch), scratch.numel(), _stream(stream))
     _check("comet_w4ax_linear", st)
+    if sync and not Y.is_cuda:
+        (stream if stream is not None else torch.cuda.current_stream()).synchronize()
     return Y
 
 

@@ -28,6 +28,8 @@ std::atomic<int64_t> g_launches{0};
 // tools only (comet_debug_set_pf_clusters): CTA pairs of the prefill grid,
 // 0 = one persistent pair per SM pair (the product schedule)
 std::atomic<int> g_pf_clusters{0};
+// tools only (comet_debug_set_pf_group): token tiles per raster group, 0 = by L2 budget
+std::atomic<int> g_pf_group{0};
 
 comet_status cuda_fail(cudaError_t e) {
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
@@ -218,7 +220,17 @@ comet_status launch_gemm_pf(const CUtensorMap& tmXe, const CUtensorMap& tmX8, co
   if (attr_err != cudaSuccess) return cuda_fail(attr_err);
   PfSched sched;
   sched.m_tiles = p.m_tiles;
+  sched.n_tiles = p.n_tiles;
   sched.tiles = p.m_tiles * p.n_tiles;
+  // raster group: as many 256-row token tiles (256 x K operand bytes each) as
+  // fit in ~48 MB of the 126 MB L2, so the group's tokens are read from HBM
+  // once while the weight tiles stream past (LLaMA-3-8B down projection,
+  // K = 14336: one group of all 32 token tiles re-read the 117 MB token plane
+  // ~10x, 1.26 GB of DRAM reads per launch)
+  const int64_t budget = 48ll << 20;
+  int gm = (int)std::min<int64_t>(p.m_tiles, std::max<int64_t>(1, budget / (256ll * args.K)));
+  if (g_pf_group.load(std::memory_order_relaxed) > 0) gm = std::min(p.m_tiles, g_pf_group.load());
+  sched.group_m = gm;
   const int want = g_pf_clusters.load(std::memory_order_relaxed) > 0 ? g_pf_clusters.load() : p.clusters;
   sched.clusters = sched.tiles < want ? sched.tiles : want;
   // PDL: the prologue (barrier init, TMEM allocation) overlaps the token
@@ -389,7 +401,13 @@ comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, in
 constexpr int kLinMaxChunks = 8;
 struct LinStreams {
   cudaStream_t in, out;
-  cudaEvent_t ev_start, ev_end, ev_end2, ev_in[kLinMaxChunks], ev_out[kLinMaxChunks];
+  cudaEvent_t ev_start, ev_end, ev_end2, ev_compute, ev_in[kLinMaxChunks], ev_out[kLinMaxChunks];
+  // the previous host-buffer call on this device: its stream, whether its
+  // output copies are ordered only by ev_end, and the device range of its
+  // staged Y (which those copies read)
+  bool prev_valid = false;
+  cudaStream_t prev_stream = nullptr;
+  uintptr_t prev_ys_lo = 0, prev_ys_hi = 0;
 };
 LinStreams* lin_streams() {
   static LinStreams g_ls[64];
@@ -403,7 +421,8 @@ LinStreams* lin_streams() {
               cudaStreamCreateWithFlags(&L.out, cudaStreamNonBlocking) == cudaSuccess &&
               cudaEventCreateWithFlags(&L.ev_start, cudaEventDisableTiming) == cudaSuccess &&
               cudaEventCreateWithFlags(&L.ev_end, cudaEventDisableTiming) == cudaSuccess &&
-              cudaEventCreateWithFlags(&L.ev_end2, cudaEventDisableTiming) == cudaSuccess;
+              cudaEventCreateWithFlags(&L.ev_end2, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&L.ev_compute, cudaEventDisableTiming) == cudaSuccess;
     for (int c = 0; c < kLinMaxChunks && ok; ++c)
       ok = cudaEventCreateWithFlags(&L.ev_in[c], cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&L.ev_out[c], cudaEventDisableTiming) == cudaSuccess;
@@ -638,7 +657,12 @@ comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K,
                            wsb > 0 ? (size_t)wsb : 0, stream);
   };
 
-  if (!x_host && !y_host) return layer(X, ldx, M, Y, ldy);
+  if (!x_host && !y_host) {
+    // a device-buffer call may use scratch bytes a later host-buffer call
+    // stages into: that call must order its input copies after this one
+    if (LinStreams* ls = lin_streams()) ls->prev_valid = false;
+    return layer(X, ldx, M, Y, ldy);
+  }
 
   // host buffers: row chunks pipeline H2D (copy stream) / compute (stream) /
   // D2H (copy stream), so the PCIe transfers in both directions overlap the
@@ -650,10 +674,21 @@ comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K,
   std::vector<int> edges(nch + 1);
   for (int c = 0; c <= nch; ++c) edges[c] = (int)(((int64_t)M * c / nch + 255) / 256 * 256);
   edges[nch] = M;
-  e = cudaEventRecord(ls->ev_start, st);  // the copies follow the caller's earlier work on st
-  if (e != cudaSuccess) return cuda_fail(e);
-  if ((e = cudaStreamWaitEvent(ls->in, ls->ev_start, 0)) != cudaSuccess) return cuda_fail(e);
-  if ((e = cudaStreamWaitEvent(ls->out, ls->ev_start, 0)) != cudaSuccess) return cuda_fail(e);
+  // input copies: after the caller's earlier work on st -- except right after
+  // a host-buffer call on the same stream, whose tail makes st wait for its
+  // output copies: then only after that call's compute (and its output
+  // copies only if this call's staged X overlaps the Y they read), so this
+  // call's H2D overlaps the previous call's D2H
+  const uintptr_t xs_lo = reinterpret_cast<uintptr_t>(xs), xs_hi = xs_lo + (x_host ? (uintptr_t)M * K * 2 : 0);
+  if (ls->prev_valid && ls->prev_stream == st) {
+    if ((e = cudaStreamWaitEvent(ls->in, ls->ev_compute, 0)) != cudaSuccess) return cuda_fail(e);
+    if (x_host && xs_lo < ls->prev_ys_hi && ls->prev_ys_lo < xs_hi &&
+        (e = cudaStreamWaitEvent(ls->in, ls->ev_end, 0)) != cudaSuccess)
+      return cuda_fail(e);
+  } else {
+    if ((e = cudaEventRecord(ls->ev_start, st)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaStreamWaitEvent(ls->in, ls->ev_start, 0)) != cudaSuccess) return cuda_fail(e);
+  }
   for (int c = 0; c < nch; ++c) {
     const int m0 = edges[c], mc = edges[c + 1] - m0;
     if (mc <= 0) continue;
@@ -680,12 +715,17 @@ comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K,
       if (e != cudaSuccess) return cuda_fail(e);
     }
   }
-  // later work on st orders after the copies; host Y is complete on return
+  // later work on st (and a synchronisation of st) orders after the copies;
+  // the call itself does not wait: host Y is complete once st is synchronised
+  if ((e = cudaEventRecord(ls->ev_compute, st)) != cudaSuccess) return cuda_fail(e);
   if ((e = cudaEventRecord(ls->ev_end, ls->out)) != cudaSuccess) return cuda_fail(e);
   if ((e = cudaStreamWaitEvent(st, ls->ev_end, 0)) != cudaSuccess) return cuda_fail(e);
   if ((e = cudaEventRecord(ls->ev_end2, ls->in)) != cudaSuccess) return cuda_fail(e);
   if ((e = cudaStreamWaitEvent(st, ls->ev_end2, 0)) != cudaSuccess) return cuda_fail(e);
-  if (y_host && (e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e);
+  ls->prev_valid = true;
+  ls->prev_stream = st;
+  ls->prev_ys_lo = reinterpret_cast<uintptr_t>(ys);
+  ls->prev_ys_hi = ls->prev_ys_lo + (y_host ? (uintptr_t)M * N * 2 : 0);
   return COMET_OK;
 }
 
@@ -993,6 +1033,12 @@ int64_t comet_launch_count(void) { return g_launches.load(); }
 // schedule); 0 restores the persistent grid.  Results are identical.
 int comet_debug_set_pf_clusters(int n) {
   g_pf_clusters.store(n < 0 ? 0 : n);
+  return 0;
+}
+// Raster ablation: token tiles per group of the prefill tile order (0 = the
+// L2-budget rule).  Results are identical.
+int comet_debug_set_pf_group(int n) {
+  g_pf_group.store(n < 0 ? 0 : n);
   return 0;
 }
 

@@ -167,12 +167,19 @@ struct PfCfg {
   static constexpr int kTemptyCount = 2 * kPWarps;  // both CTAs' promotion warps
 };
 
+// Tile order: groups of group_m token tiles; inside a group the token tile
+// runs fastest, then the weight tile.  The host sizes group_m so the group's
+// token rows stay resident in L2 while every weight tile passes over them
+// (group_m = m_tiles: one group, token tiles fastest, each weight tile read
+// once; group_m = 1: weight tiles fastest, each token tile read once).
 struct PfSched {
-  int m_tiles, tiles, clusters;
+  int m_tiles, n_tiles, tiles, clusters, group_m;
   DEVI void coords(int t, int& m0, int& n0) const {
-    const int mt = t % m_tiles;  // token tiles fastest: concurrent clusters share weight tiles in L2
-    m0 = mt * 256;
-    n0 = (t / m_tiles) * PfCfg::kTileN;
+    const int per = group_m * n_tiles;
+    const int g = t / per, r = t - g * per;
+    const int gm = min(group_m, m_tiles - g * group_m);
+    m0 = (g * group_m + r % gm) * 256;
+    n0 = (r / gm) * PfCfg::kTileN;
   }
 };
 

@@ -317,6 +317,45 @@ def test_linear_prefill_fused_quantizer(M, K, n8, group):
     assert np.array_equal(Y.cpu().numpy().view(np.uint16), ref.view(np.uint16))
 
 
+def test_linear_host_calls_overlap_without_sync():
+    """Consecutive host-buffer calls (sync=False) overlap their copies: the
+    input copies of a call start after the previous call's compute, not its
+    output copies.  Same scratch reused by calls of different shapes (the
+    second call's staged X overlaps the first call's staged Y, so that case
+    must wait for the first call's output copies), a separate scratch, and a
+    device-buffer call in between; every Y must equal its device-buffer
+    result after one synchronize."""
+    cases = [(2600, 640, 1024, 2, 41), (2300, 1024, 2048, 3, 42), (2100, 512, 1152, 3, 43)]
+    shared = None
+    jobs = []
+    for i, (M, N, K, n8, seed) in enumerate(cases):
+        p = synth.make_problem(M, N, K, n8=n8, seed=seed, mask="scattered")
+        W, perm = to_dev(p["W"]), to_dev(p["perm"])
+        bits = comet.BlockBits(p["bits"])
+        Wq, Sw = comet.comet_pack_weight(W, perm, 128)
+        need = comet.comet_w4ax_linear_scratch_bytes(M, N, K, bits)
+        own = comet.new_workspace(need, W.device)
+        ref = comet.comet_w4ax_linear(to_dev(p["X"]), bits, Wq, Sw, perm=perm, scratch=own).cpu().numpy()
+        jobs.append((p, bits, Wq, Sw, perm, M, N, own, ref))
+    need = max(comet.comet_w4ax_linear_scratch_bytes(j[5], j[6], j[0]["X"].shape[1], j[1]) for j in jobs)
+    shared = comet.new_workspace(need, jobs[0][2].device)
+    torch.cuda.synchronize()
+    outs = []
+    for i, (p, bits, Wq, Sw, perm, M, N, own, ref) in enumerate(jobs):
+        Xh = torch.from_numpy(p["X"]).pin_memory()
+        Yh = torch.full((M, N), float("nan"), dtype=torch.float16).pin_memory()
+        scratch = own if i == 1 else shared
+        comet.comet_w4ax_linear(Xh, bits, Wq, Sw, perm=perm, out=Yh, scratch=scratch, sync=False)
+        if i == 1:  # a device-buffer call on the shared scratch between host calls
+            pd = jobs[0]
+            dev_y = comet.comet_w4ax_linear(to_dev(pd[0]["X"]), pd[1], pd[2], pd[3], perm=pd[4], scratch=shared)
+            outs.append((dev_y, pd[8]))
+        outs.append((Yh, ref))
+    torch.cuda.synchronize()
+    for Y, ref in outs:
+        assert np.array_equal(Y.cpu().numpy().view(np.uint16), ref.view(np.uint16))
+
+
 def test_linear_host_buffers_pipelined_chunks():
     """Host X and Y at M >= 2048: the call pipelines row chunks (H2D / layer /
     D2H on internal copy streams); Y must equal the device-buffer call."""
