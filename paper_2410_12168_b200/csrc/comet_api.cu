@@ -447,7 +447,8 @@ int64_t plane_bytes(int32_t M, int32_t K, const uint8_t* bits, int want) {
 template <bool kBf16>
 comet_status quantize_act_impl(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
                                const uint8_t* block_bits, int8_t* Xq8, void* Xq4, float* Sx, int64_t ldsx,
-                               comet_stream_t stream, uint8_t* X4e = nullptr, float* CX = nullptr) {
+                               comet_stream_t stream, uint8_t* X4e = nullptr, float* CX = nullptr,
+                               const uint16_t* perm16 = nullptr) {
   if (M < 0 || K <= 0 || !block_bits) return COMET_ERR_INVALID_ARG;
   if (K % 128 || K > 65536 || ldx < K || ldx % 8 || ldsx < M || ldsx % 4) return COMET_ERR_SHAPE;
   BlockMap map;
@@ -467,8 +468,11 @@ comet_status quantize_act_impl(const void* X, int64_t ldx, int32_t M, int32_t K,
     // row-staged kernel: persistent CTAs, double-buffered rows in smem
     const int smem = kQNBuf * K * 2;  // row buffers
     if (smem <= 200 * 1024) {
-      auto kern = X4e ? (perm ? quantize_act_rows_kernel<true, false, kBf16, true> : quantize_act_rows_kernel<false, false, kBf16, true>)
-                      : (perm ? quantize_act_rows_kernel<true, false, kBf16> : quantize_act_rows_kernel<false, false, kBf16>);
+      auto kern = X4e ? (perm16 ? quantize_act_rows_kernel<2, false, kBf16, true>
+                                : perm ? quantize_act_rows_kernel<1, false, kBf16, true>
+                                       : quantize_act_rows_kernel<0, false, kBf16, true>)
+                      : (perm ? quantize_act_rows_kernel<1, false, kBf16> : quantize_act_rows_kernel<0, false, kBf16>);
+      const int32_t* pk = (X4e && perm16) ? reinterpret_cast<const int32_t*>(perm16) : perm;
       // (dynamic smem above the 48 KB default needs the opt-in; set per call,
       // it is a cheap host-side attribute)
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -481,7 +485,7 @@ comet_status quantize_act_impl(const void* X, int64_t ldx, int32_t M, int32_t K,
       if (per_sm < 1) per_sm = 1;
       int64_t grid = (int64_t)num_sms * per_sm;
       if (grid > ldsx) grid = ldsx;
-      kern<<<(int)grid, kQThreads, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
+      kern<<<(int)grid, kQThreads, smem, st>>>(Xh, ldx, M, K / 128, ldsx, pk, map, Xq8, (int64_t)n8 * 128,
                                          X4e ? X4e : reinterpret_cast<uint8_t*>(Xq4),
                                          X4e ? (int64_t)n4 * 128 : (int64_t)n4 * 64, Sx, nullptr, CX);
       return check_launch();
@@ -521,6 +525,7 @@ int64_t comet_w4ax_linear_scratch_bytes(int32_t M, int32_t N, int32_t K, const u
   if (p8 < 0 || p4 < 0 || ws < 0) return -1;
   int64_t sx = (K / 128) * comet_act_ldsx(M) * 4;
   int64_t io = align256((int64_t)M * K * 2) + align256((int64_t)M * N * 2);  // staging for host X / Y
+  io += align256((int64_t)K * 2);  // the permutation as uint16 (quantizer)
   // the GEMM workspace sits at the scratch base and is never shorter than the
   // stream-K tile counters, so a prefill call (no workspace) never overwrites
   // the counters a later decode call on the same scratch relies on
@@ -628,6 +633,10 @@ comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K,
   p += align256(p4);
   float* Sx = reinterpret_cast<float*>(p);
   p += align256((K / 128) * comet_act_ldsx(M) * 4);
+  // the permutation as uint16 for the row-staged quantizer (prefill layers)
+  const bool use16 = perm && M > 128 && (int64_t)kQNBuf * K * 2 <= 200 * 1024;
+  uint16_t* perm16 = use16 ? reinterpret_cast<uint16_t*>(p) : nullptr;
+  p += align256((int64_t)K * 2);
   char* xs = nullptr;  // host X staged densely (ld = K)
   if (x_host) {
     xs = p;
@@ -646,7 +655,7 @@ comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K,
       uint8_t* x4e = reinterpret_cast<uint8_t*>(ws) + kCounterBytes;
       float* cx = reinterpret_cast<float*>(x4e + align256((int64_t)mc * K));
       comet_status s = quantize_act_impl<false>(Xd, ldxd, mc, K, perm, block_bits, Xq8, nullptr, Sx, ldsx, stream,
-                                                x4e, cx);
+                                                x4e, cx, perm16);
       if (s != COMET_OK) return s;
       return gemm_common(Xq8, nullptr, Sx, ldsx, block_bits, mc, K, Wq, Sw, N, group, Yd, ldyd, nullptr, ws,
                          (size_t)wsb, st, true);
@@ -657,6 +666,11 @@ comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K,
                            wsb > 0 ? (size_t)wsb : 0, stream);
   };
 
+  if (perm16) {
+    perm_to_u16_kernel<<<(K + 255) / 256, 256, 0, st>>>(perm, K, perm16);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
   if (!x_host && !y_host) {
     // a device-buffer call may use scratch bytes a later host-buffer call
     // stages into: that call must order its input copies after this one
@@ -917,7 +931,7 @@ comet_status comet_quantize_act_static(const void* X, int64_t ldx, int32_t M, in
   if (M >= 64 && kQNBuf * K * 2 <= 200 * 1024) {
     // row-staged kernel (as comet_quantize_act), static-scale arithmetic
     const int smem = kQNBuf * K * 2;
-    auto kern = perm ? quantize_act_rows_kernel<true, true> : quantize_act_rows_kernel<false, true>;
+    auto kern = perm ? quantize_act_rows_kernel<1, true> : quantize_act_rows_kernel<0, true>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_fail(e);
     int per_sm = 0;  // one wave of persistent CTAs
@@ -929,11 +943,11 @@ comet_status comet_quantize_act_static(const void* X, int64_t ldx, int32_t M, in
     int64_t g = (int64_t)num_sms * per_sm;
     if (g > ldsx) g = ldsx;
     if (perm)
-      quantize_act_rows_kernel<true, true><<<(int)g, kQThreads, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8,
+      quantize_act_rows_kernel<1, true><<<(int)g, kQThreads, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8,
                                                                       (int64_t)n8 * 128, reinterpret_cast<uint8_t*>(Xq4),
                                                                       (int64_t)n4 * 64, Sx, scales);
     else
-      quantize_act_rows_kernel<false, true><<<(int)g, kQThreads, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8,
+      quantize_act_rows_kernel<0, true><<<(int)g, kQThreads, smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8,
                                                                        (int64_t)n8 * 128, reinterpret_cast<uint8_t*>(Xq4),
                                                                        (int64_t)n4 * 64, Sx, scales);
     return check_launch();

@@ -289,7 +289,12 @@ constexpr int kQNBuf = COMET_Q_NBUF;
 //   INT8 / packed INT4: h = (copysign(t - M, x)) + M, low byte = q.
 // A negative x with q == 0 gives the e4m3 byte 0x80 (-0.0): its products
 // add exactly zero in the GEMM, the same as +0.
-template <int kL, bool kPerm, bool kStatic = false, bool kBf16 = false, bool kE4 = false>
+// kPerm: 0 = no permutation, 1 = int32 perm (the API's), 2 = the same
+// permutation as uint16 (comet_w4ax_linear converts it once per call into its
+// scratch: half the bytes, so a K = 14336 permutation (28 KB) stays in L1
+// next to the row buffers, where the int32 one (57 KB) was re-read from L2
+// for every row)
+template <int kL, int kPerm, bool kStatic = false, bool kBf16 = false, bool kE4 = false>
 DEVI void quant_item(const unsigned short* row, const int32_t* __restrict__ gperm, const BlockMap& map, int b, bool valid,
                      int o, int64_t m, int64_t ldsx, int8_t* __restrict__ Xq8, int64_t ld8, uint8_t* __restrict__ Xq4,
                      int64_t ld4, float* __restrict__ Sx, const float* __restrict__ sstat = nullptr,
@@ -299,7 +304,16 @@ DEVI void quant_item(const unsigned short* row, const int32_t* __restrict__ gper
   constexpr int kLanes = 128 / kL;       // lanes per item
   const int i0 = b * 128 + o * kL;
   uint32_t w[kW];  // elements 2j (low half) and 2j + 1 (high half)
-  if (kPerm) {
+  if (kPerm == 2) {
+    const uint16_t* p16 = reinterpret_cast<const uint16_t*>(gperm);
+#pragma unroll
+    for (int v = 0; v < kL / 8; ++v) {
+      const uint4 u = __ldg(reinterpret_cast<const uint4*>(p16 + i0) + v);
+      const uint32_t pw[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) w[4 * v + j] = __byte_perm(row[pw[j] & 0xFFFF], row[pw[j] >> 16], 0x5410);
+    }
+  } else if (kPerm) {
 #pragma unroll
     for (int v = 0; v < kL / 4; ++v) {
       const int4 p = __ldg(reinterpret_cast<const int4*>(gperm + i0) + v);
@@ -422,7 +436,7 @@ DEVI void quant_item(const unsigned short* row, const int32_t* __restrict__ gper
 #define COMET_Q_THREADS 256
 #endif
 constexpr int kQThreads = COMET_Q_THREADS;  // threads per CTA of the row-staged kernel
-template <bool kPerm, bool kStatic = false, bool kBf16 = false, bool kE4 = false>
+template <int kPerm, bool kStatic = false, bool kBf16 = false, bool kE4 = false>
 __global__ void __launch_bounds__(kQThreads, COMET_Q_MINB) quantize_act_rows_kernel(const __half* __restrict__ X, int64_t ldx, int M,
                                                                 int nb, int64_t ldsx, const int32_t* __restrict__ perm,
                                                                 const __grid_constant__ BlockMap map,
@@ -492,6 +506,13 @@ __global__ void __launch_bounds__(kQThreads, COMET_Q_MINB) quantize_act_rows_ker
                                                  ld8, Xq4, ld4, Sx, sstat, &tab, CX);
     __syncthreads();  // every lane group is done with this buffer
   }
+}
+
+// perm int32[K] -> uint16[K] (K <= 65536), for the quantizer's kPerm == 2 path
+__global__ void __launch_bounds__(256) perm_to_u16_kernel(const int32_t* __restrict__ perm, int K,
+                                                          uint16_t* __restrict__ out) {
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i < K) out[i] = (uint16_t)__ldg(perm + i);
 }
 
 // Weight pack with one scale per output channel (group == K): a warp per
