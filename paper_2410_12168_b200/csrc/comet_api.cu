@@ -17,6 +17,7 @@
 #include "fmpq_aux.cuh"
 #include "gemm_decode.cuh"
 #include "quantize.cuh"
+#include "quantize_lane.cuh"
 #include "tp.cuh"
 
 using namespace comet;
@@ -464,6 +465,22 @@ comet_status quantize_act_impl(const void* X, int64_t ldx, int32_t M, int32_t K,
   if (ds != COMET_OK) return ds;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const __half* Xh = reinterpret_cast<const __half*>(X);
+  if (M >= kLaneMinRows) {
+    // thread-per-item kernel (quantize_lane.cuh): persistent, one CTA per SM
+    const LanePlan lp = lane_plan(M, K, perm != nullptr);
+    if (lp.S) {
+      auto kern = X4e ? (perm ? quantize_lane_kernel<true, kBf16, true> : quantize_lane_kernel<true, kBf16, false>)
+                      : (perm ? quantize_lane_kernel<false, kBf16, true> : quantize_lane_kernel<false, kBf16, false>);
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lp.smem);
+      if (e != cudaSuccess) return cuda_fail(e);
+      const int64_t grid = std::min<int64_t>(num_sms, lp.stages);
+      kern<<<(int)grid, lp.threads, lp.smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
+                                                    X4e ? X4e : reinterpret_cast<uint8_t*>(Xq4),
+                                                    X4e ? (int64_t)n4 * 128 : (int64_t)n4 * 64, Sx, CX, lp.R, lp.S,
+                                                    lp.lpr);
+      return check_launch();
+    }
+  }
   if (M >= 64) {
     // row-staged kernel: persistent CTAs, double-buffered rows in smem
     const int smem = kQNBuf * K * 2;  // row buffers
@@ -634,7 +651,7 @@ comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K,
   float* Sx = reinterpret_cast<float*>(p);
   p += align256((K / 128) * comet_act_ldsx(M) * 4);
   // the permutation as uint16 for the row-staged quantizer (prefill layers)
-  const bool use16 = perm && M > 128 && (int64_t)kQNBuf * K * 2 <= 200 * 1024;
+  const bool use16 = perm && M > 128 && (int64_t)kQNBuf * K * 2 <= 200 * 1024 && !(M >= kLaneMinRows && lane_plan(M, K, true).S);
   uint16_t* perm16 = use16 ? reinterpret_cast<uint16_t*>(p) : nullptr;
   p += align256((int64_t)K * 2);
   char* xs = nullptr;  // host X staged densely (ld = K)
