@@ -140,6 +140,33 @@ comet_status comet_w4ax_gemm(const int8_t* Xq8, const void* Xq4, const float* Sx
 comet_status comet_gather_shards(const void* Yall, int32_t P, int32_t M, int32_t per, int32_t N, void* Y,
                                  int64_t ldy, comet_stream_t stream);
 
+/* ---- f1: GEMM with the all-gather fused into its epilogue (§4.4:
+ * "the all-gather ... overlapped with the GEMM", BJ north_star) ------------
+ * Rank r of P computes its N-shard Y_r = comet_w4ax_gemm(...) [M x N] and
+ * the epilogue writes every Y_r element into ALL nY destinations: Ys[i] is a
+ * full-width output [M x ldy] fp16 (row stride ldy, ldy >= col0 + N,
+ * ldy % 8 == 0) and Y_r lands in its columns [col0, col0 + N) (col0 % 8 ==
+ * 0, normally r * N).  Ys[0] is this GPU's copy; Ys[1 ..] are other ranks'
+ * copies mapped into this process (CUDA IPC / symmetric memory over NVLink:
+ * the stores leave this GPU as P2P writes from the TMA engine, tile by tile,
+ * overlapping the remaining tiles' MMAs).  1 <= nY <= 8; every Ys[i] 16-byte
+ * aligned and writable from the current device.  The call only enqueues:
+ * the caller's single cross-rank barrier after it (e.g. the symmetric-memory
+ * barrier) makes every rank's copy complete.  Other arguments as for
+ * comet_w4ax_gemm. */
+comet_status comet_w4ax_gemm_allgather(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
+                                       const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq,
+                                       const float* Sw, int32_t N, int32_t group, void* const* Ys, int32_t nY,
+                                       int64_t ldy, int64_t col0, void* workspace, size_t workspace_bytes,
+                                       comet_stream_t stream);
+/* the whole layer (quantize_act + the fused GEMM above); X and every Ys[i]
+ * DEVICE pointers (COMET_ERR_INVALID_ARG for host buffers); scratch as for
+ * comet_w4ax_linear. */
+comet_status comet_w4ax_linear_allgather(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
+                                         const uint8_t* block_bits, const void* Wq, const float* Sw, int32_t N,
+                                         int32_t group, void* const* Ys, int32_t nY, int64_t ldy, int64_t col0,
+                                         void* scratch, size_t scratch_bytes, comet_stream_t stream);
+
 /* ---- test/debug: per-block INT32 accumulators ---------------------------
  * Acc int32 [K/128 x M x N]: Acc[(b*M + m)*N + n] = sum_{i in block b}
  * xq[m,i]*wq[n,i] in LOGICAL units (the x16 zero-extension factor and, in

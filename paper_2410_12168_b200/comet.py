@@ -25,7 +25,8 @@ EXPORTS = ["comet_act_plane8_bytes", "comet_act_plane4_bytes", "comet_act_ldsx",
            "comet_w4ax_linear_scratch_bytes", "comet_pack_weight", "comet_quantize_act", "comet_w4ax_gemm",
            "comet_w4ax_gemm_acc_i32", "comet_w4ax_linear", "comet_calib_absmax", "comet_fmpq_map",
            "comet_quantize_kv", "comet_dequantize_kv", "comet_static_act_scales", "comet_quantize_act_static",
-           "comet_quantize_act_bf16", "comet_gather_shards", "comet_attention_kv4",
+           "comet_quantize_act_bf16", "comet_gather_shards", "comet_w4ax_gemm_allgather",
+           "comet_w4ax_linear_allgather", "comet_attention_kv4",
            "comet_pack_weight_f16s", "comet_w4ax_gemm_f16s", "comet_w4ax_gemm_f16s_workspace_bytes",
            "comet_attention_kv4_workspace_bytes",
            "comet_status_str", "comet_last_cuda_error",
@@ -93,6 +94,11 @@ def lib():
         L.comet_attention_kv4.restype = ctypes.c_int
         L.comet_gather_shards.argtypes = [P, i32, i32, i32, i32, P, i64, P]
         L.comet_gather_shards.restype = ctypes.c_int
+        L.comet_w4ax_gemm_allgather.argtypes = [P, P, P, i64, P, i32, i32, P, P, i32, i32, P, i32, i64, i64, P,
+                                                sz, P]
+        L.comet_w4ax_gemm_allgather.restype = ctypes.c_int
+        L.comet_w4ax_linear_allgather.argtypes = [P, i64, i32, i32, P, P, P, P, i32, i32, P, i32, i64, i64, P, sz, P]
+        L.comet_w4ax_linear_allgather.restype = ctypes.c_int
         L.comet_quantize_act_bf16.argtypes = [P, i64, i32, i32, P, P, P, P, P, i64, P]
         L.comet_quantize_act_bf16.restype = ctypes.c_int
         L.comet_static_act_scales.argtypes = [P, i32, P, P, P, P]
@@ -409,6 +415,48 @@ def comet_w4ax_linear(X: torch.Tensor, bits, Wq, Sw, perm=None, group: int = BLO
     if sync and not Y.is_cuda:
         (stream if stream is not None else torch.cuda.current_stream()).synchronize()
     return Y
+
+
+def _dest_array(dests):
+    """f1 destinations: tensors (this process's buffers) or raw device
+    addresses (peers' buffers mapped into this process) -> void*[]"""
+    ptrs = [d.data_ptr() if isinstance(d, torch.Tensor) else int(d) for d in dests]
+    return (ctypes.c_void_p * len(ptrs))(*ptrs), len(ptrs)
+
+
+def comet_w4ax_gemm_allgather(Xq8, Xq4, Sx, bits, Wq, Sw, dests, ldy: int, col0: int, group: int = BLOCK,
+                              workspace: Optional[torch.Tensor] = None, stream=None):
+    """f1: the GEMM's epilogue writes its [M x N] result into columns
+    [col0, col0 + N) of every destination [M x ldy] fp16 (dests[0] local,
+    the rest peers' copies); the caller's cross-rank barrier follows."""
+    b = as_bits(bits)
+    M = Xq8.shape[0] if b.n8 else Xq4.shape[0]
+    N, K = Wq.shape[0], Wq.shape[1] * 2
+    need = comet_w4ax_gemm_workspace_bytes(M, N, K)
+    if need > 0 and (workspace is None or workspace.numel() < need):
+        raise CometError("comet_w4ax_gemm_allgather", 4)
+    arr, n = _dest_array(dests)
+    st = lib().comet_w4ax_gemm_allgather(_ptr(Xq8) if b.n8 else None, _ptr(Xq4) if b.n4 else None, _ptr(Sx),
+                                         Sx.shape[1], b.ptr, M, K, _ptr(Wq), _ptr(Sw), N, group, arr, n, ldy, col0,
+                                         _ptr(workspace), 0 if workspace is None else workspace.numel(),
+                                         _stream(stream))
+    _check("comet_w4ax_gemm_allgather", st)
+
+
+def comet_w4ax_linear_allgather(X: torch.Tensor, bits, Wq, Sw, dests, ldy: int, col0: int, perm=None,
+                                group: int = BLOCK, scratch: Optional[torch.Tensor] = None, stream=None):
+    """f1: the whole layer with the all-gather fused into the GEMM epilogue
+    (device buffers only); see comet_w4ax_gemm_allgather."""
+    b = as_bits(bits)
+    M, K = X.shape
+    N = Wq.shape[0]
+    need = comet_w4ax_linear_scratch_bytes(M, N, K, b)
+    if scratch is None or scratch.numel() < need:
+        raise CometError("comet_w4ax_linear_allgather", 4)
+    arr, n = _dest_array(dests)
+    st = lib().comet_w4ax_linear_allgather(_ptr(X), X.stride(0), M, K, _ptr(perm), b.ptr, _ptr(Wq), _ptr(Sw), N,
+                                           group, arr, n, ldy, col0, _ptr(scratch), scratch.numel(), _stream(stream))
+    _check("comet_w4ax_linear_allgather", st)
 
 
 class W4AxLinear:

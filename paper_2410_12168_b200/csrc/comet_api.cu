@@ -213,7 +213,8 @@ Plan make_plan(int M, int N, int K, int num_sms) {
 
 template <bool kGroupK, bool kAcc>
 comet_status launch_gemm_pf(const CUtensorMap& tmXe, const CUtensorMap& tmX8, const CUtensorMap& tmY,
-                            const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
+                            const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st,
+                            const YPeerMaps& yp) {
   using C = PfCfg;
   auto kern = w4ax_gemm_pf_kernel<kGroupK, kAcc>;
   static AttrCache cache;
@@ -237,7 +238,7 @@ comet_status launch_gemm_pf(const CUtensorMap& tmXe, const CUtensorMap& tmX8, co
   // PDL: the prologue (barrier init, TMEM allocation) overlaps the token
   // preparation kernel; the producers wait for it before their first load
   cudaError_t e = launch_pdl(kern, dim3(2 * sched.clusters), dim3(C::kThreads), C::kSmemBytes, st, tmXe, tmX8, tmY,
-                             map, args, sched);
+                             map, args, sched, yp);
   if (e != cudaSuccess) return cuda_fail(e);
   return check_launch();
 }
@@ -294,11 +295,12 @@ comet_status launch_decode_bn(const CUtensorMap& tmX4, const CUtensorMap& tmX8, 
 
 template <bool kAcc>
 comet_status launch_gemm(const CUtensorMap& tmXp, const CUtensorMap& tmX8, const CUtensorMap& tmY,
-                         const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st) {
+                         const BlockMap& map, const GemmArgs& args, const Plan& p, cudaStream_t st,
+                         const YPeerMaps& yp) {
   const bool group_k = args.group_blocks == args.nb;
   if (p.two_sm) {
-    if (group_k) return launch_gemm_pf<true, kAcc>(tmXp, tmX8, tmY, map, args, p, st);
-    return launch_gemm_pf<false, kAcc>(tmXp, tmX8, tmY, map, args, p, st);
+    if (group_k) return launch_gemm_pf<true, kAcc>(tmXp, tmX8, tmY, map, args, p, st, yp);
+    return launch_gemm_pf<false, kAcc>(tmXp, tmX8, tmY, map, args, p, st, yp);
   }
   if (group_k) return launch_decode_bn<true, kAcc>(tmXp, tmX8, map, args, p, st);
   return launch_decode_bn<false, kAcc>(tmXp, tmX8, map, args, p, st);
@@ -307,7 +309,7 @@ comet_status launch_gemm(const CUtensorMap& tmXp, const CUtensorMap& tmX8, const
 comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx, const uint8_t* bits,
                          int32_t M, int32_t K, const void* Wq, const float* Sw, int32_t N, int32_t group, void* Y,
                          int64_t ldy, int32_t* Acc, void* ws, size_t ws_bytes, cudaStream_t st,
-                         bool prepared = false) {
+                         bool prepared = false, void* const* ypeers = nullptr, int npeer = 0) {
   // prepared (comet_w4ax_linear): the quantizer already wrote the prefill
   // kernel's e4m3 token plane and corrections into the workspace (Xq4 unused)
   if (!bits || M < 0 || N < 0 || K <= 0) return COMET_ERR_INVALID_ARG;
@@ -363,7 +365,22 @@ comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, in
     if (!make_map_u8(&tmY, Y, (uint64_t)N * 2, (uint64_t)M, (uint64_t)ldy * 2, 64, 32, CU_TENSOR_MAP_SWIZZLE_64B))
       return map_fail("Y");
   }
+  // f1: the peers' copies of the output take every Y store too
+  if (npeer < 0 || npeer > kMaxYPeers || (npeer && (!ypeers || Acc))) return COMET_ERR_INVALID_ARG;
+  YPeerMaps yp;
+  memset(&yp, 0, sizeof(yp));
+  yp.n = npeer;
+  for (int i = 0; i < npeer; ++i) {
+    if (!ypeers[i]) return COMET_ERR_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(ypeers[i]) & 15) return COMET_ERR_ALIGNMENT;
+    if (p.two_sm && !make_map_u8(&yp.m[i], ypeers[i], (uint64_t)N * 2, (uint64_t)M, (uint64_t)ldy * 2, 64, 32,
+                                 CU_TENSOR_MAP_SWIZZLE_64B))
+      return map_fail("Y peer");
+  }
   GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.npeer = npeer;
+  for (int i = 0; i < npeer; ++i) a.Ypeer[i] = reinterpret_cast<__half*>(ypeers[i]);
   a.M = M;
   a.N = N;
   a.K = K;
@@ -391,8 +408,8 @@ comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, in
     comet_status ls = check_launch();
     if (ls != COMET_OK) return ls;
   }
-  if (Acc) return launch_gemm<true>(tmXp, tmX8, tmY, map, a, p, st);
-  return launch_gemm<false>(tmXp, tmX8, tmY, map, a, p, st);
+  if (Acc) return launch_gemm<true>(tmXp, tmX8, tmY, map, a, p, st, yp);
+  return launch_gemm<false>(tmXp, tmX8, tmY, map, a, p, st, yp);
 }
 
 // comet_w4ax_linear with host buffers: two internal copy streams and their
@@ -612,10 +629,14 @@ comet_status comet_w4ax_gemm_acc_i32(const int8_t* Xq8, const void* Xq4, const f
                      workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
-comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
-                               const uint8_t* block_bits, const void* Wq, const float* Sw, int32_t N, int32_t group,
-                               void* Y, int64_t ldy, void* scratch, size_t scratch_bytes, comet_stream_t stream) {
+// comet_w4ax_linear and comet_w4ax_linear_allgather (ypeers: further
+// destinations of Y, device buffers only)
+static comet_status linear_impl(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
+                                const uint8_t* block_bits, const void* Wq, const float* Sw, int32_t N, int32_t group,
+                                void* Y, int64_t ldy, void* scratch, size_t scratch_bytes, comet_stream_t stream,
+                                void* const* ypeers, int npeer) {
   if (M < 0 || N < 0 || K <= 0 || !block_bits) return COMET_ERR_INVALID_ARG;
+  if (npeer < 0 || npeer > kMaxYPeers || (npeer && !ypeers)) return COMET_ERR_INVALID_ARG;
   if (K % 128 || N % 128 || ldx < K || ldy < N || ldx % 8 || ldy % 8) return COMET_ERR_SHAPE;
   const int64_t need = comet_w4ax_linear_scratch_bytes(M, N, K, block_bits);
   if (need < 0) return COMET_ERR_INVALID_ARG;
@@ -638,6 +659,9 @@ comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K,
   if (e != cudaSuccess) return cuda_fail(e);
   const bool x_host = ax.type != cudaMemoryTypeDevice && ax.type != cudaMemoryTypeManaged;
   const bool y_host = ay.type != cudaMemoryTypeDevice && ay.type != cudaMemoryTypeManaged;
+  if (npeer && (x_host || y_host)) return COMET_ERR_INVALID_ARG;  // the fused all-gather writes device buffers
+  for (int i = 0; i < npeer; ++i)
+    if (!ypeers[i] || (reinterpret_cast<uintptr_t>(ypeers[i]) & 15)) return COMET_ERR_ALIGNMENT;
 
   char* p = reinterpret_cast<char*>(scratch);
   const int64_t ws_bytes = comet_w4ax_gemm_workspace_bytes(M, N, K);
@@ -675,12 +699,12 @@ comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K,
                                                 x4e, cx, perm16);
       if (s != COMET_OK) return s;
       return gemm_common(Xq8, nullptr, Sx, ldsx, block_bits, mc, K, Wq, Sw, N, group, Yd, ldyd, nullptr, ws,
-                         (size_t)wsb, st, true);
+                         (size_t)wsb, st, true, ypeers, npeer);
     }
     comet_status s = comet_quantize_act(Xd, ldxd, mc, K, perm, block_bits, Xq8, Xq4, Sx, ldsx, stream);
     if (s != COMET_OK) return s;
-    return comet_w4ax_gemm(Xq8, Xq4, Sx, ldsx, block_bits, mc, K, Wq, Sw, N, group, Yd, ldyd, ws,
-                           wsb > 0 ? (size_t)wsb : 0, stream);
+    return gemm_common(Xq8, Xq4, Sx, ldsx, block_bits, mc, K, Wq, Sw, N, group, Yd, ldyd, nullptr, ws,
+                       wsb > 0 ? (size_t)wsb : 0, st, false, ypeers, npeer);
   };
 
   if (perm16) {
@@ -758,6 +782,56 @@ comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K,
   ls->prev_ys_lo = reinterpret_cast<uintptr_t>(ys);
   ls->prev_ys_hi = ls->prev_ys_lo + (y_host ? (uintptr_t)M * N * 2 : 0);
   return COMET_OK;
+}
+
+comet_status comet_w4ax_linear(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
+                               const uint8_t* block_bits, const void* Wq, const float* Sw, int32_t N, int32_t group,
+                               void* Y, int64_t ldy, void* scratch, size_t scratch_bytes, comet_stream_t stream) {
+  return linear_impl(X, ldx, M, K, perm, block_bits, Wq, Sw, N, group, Y, ldy, scratch, scratch_bytes, stream,
+                     nullptr, 0);
+}
+
+// f1: the destinations' column offset col0 applied to every pointer; Ys[0]
+// is this rank's copy, Ys[1 ..] the peers'
+static comet_status offset_dests(void* const* Ys, int32_t nY, int64_t col0, void** out) {
+  if (!Ys || nY < 1 || nY > kMaxYPeers + 1 || col0 < 0 || col0 % 8) return COMET_ERR_INVALID_ARG;
+  for (int i = 0; i < nY; ++i) {
+    if (!Ys[i]) return COMET_ERR_INVALID_ARG;
+    out[i] = reinterpret_cast<char*>(Ys[i]) + col0 * 2;
+  }
+  return COMET_OK;
+}
+
+comet_status comet_w4ax_gemm_allgather(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
+                                       const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq,
+                                       const float* Sw, int32_t N, int32_t group, void* const* Ys, int32_t nY,
+                                       int64_t ldy, int64_t col0, void* workspace, size_t workspace_bytes,
+                                       comet_stream_t stream) {
+  void* d[kMaxYPeers + 1];
+  comet_status s = offset_dests(Ys, nY, col0, d);
+  if (s != COMET_OK) return s;
+  if (ldy < col0 + N) return COMET_ERR_SHAPE;
+  return gemm_common(Xq8, Xq4, Sx, ldsx, block_bits, M, K, Wq, Sw, N, group, d[0], ldy, nullptr, workspace,
+                     workspace_bytes, reinterpret_cast<cudaStream_t>(stream), false, d + 1, nY - 1);
+}
+
+comet_status comet_w4ax_linear_allgather(const void* X, int64_t ldx, int32_t M, int32_t K, const int32_t* perm,
+                                         const uint8_t* block_bits, const void* Wq, const float* Sw, int32_t N,
+                                         int32_t group, void* const* Ys, int32_t nY, int64_t ldy, int64_t col0,
+                                         void* scratch, size_t scratch_bytes, comet_stream_t stream) {
+  void* d[kMaxYPeers + 1];
+  comet_status s = offset_dests(Ys, nY, col0, d);
+  if (s != COMET_OK) return s;
+  if (ldy < col0 + N) return COMET_ERR_SHAPE;
+  for (const void* q : {X, static_cast<const void*>(d[0])}) {  // device buffers only
+    cudaPointerAttributes at;
+    if (!q) return COMET_ERR_INVALID_ARG;
+    cudaError_t e = cudaPointerGetAttributes(&at, q);
+    if (e != cudaSuccess) return cuda_fail(e);
+    if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) return COMET_ERR_INVALID_ARG;
+  }
+  return linear_impl(X, ldx, M, K, perm, block_bits, Wq, Sw, N, group, d[0], ldy, scratch, scratch_bytes, stream,
+                     d + 1, nY - 1);
 }
 
 comet_status comet_gather_shards(const void* Yall, int32_t P, int32_t M, int32_t per, int32_t N, void* Y,

@@ -13,6 +13,11 @@
 
 namespace comet {
 
+#ifndef COMET_MAX_YPEERS
+#define COMET_MAX_YPEERS 7
+#endif
+constexpr int kMaxYPeers = COMET_MAX_YPEERS;  // f1: up to 8 ranks (this one + 7 peers)
+
 struct GemmArgs {
   int M, N, K, nb;
   int64_t ldsx, ldy;
@@ -26,6 +31,15 @@ struct GemmArgs {
   float* ws_partial;
   int* ws_counter;
   int splits;
+  // f1 (fused all-gather): further destinations of every Y element
+  // (peer GPUs' copies of the full output, P2P-mapped), same offsets as Y
+  int npeer;
+  __half* Ypeer[kMaxYPeers];
+};
+// the prefill kernel's TMA-store maps of those destinations
+struct YPeerMaps {
+  CUtensorMap m[kMaxYPeers];
+  int n;
 };
 
 // ---- debug instrumentation ------------------------------------------------

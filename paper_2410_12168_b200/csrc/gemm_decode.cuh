@@ -511,7 +511,11 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
 #pragma unroll
           for (int j = 0; j < C::kCW; ++j) {
             const int m = m0 + col0 + j;
-            if (m < args.M) args.Y[(int64_t)m * args.ldy + n] = __float2half_rn(y[j]);
+            if (m < args.M) {
+              const __half hv = __float2half_rn(y[j]);
+              args.Y[(int64_t)m * args.ldy + n] = hv;
+              for (int i = 0; i < args.npeer; ++i) args.Ypeer[i][(int64_t)m * args.ldy + n] = hv;  // f1
+            }
           }
         } else {
           // ------------------------- a7: stream-K partial + fixup ----
@@ -566,7 +570,11 @@ __global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
 #pragma unroll
             for (int j = 0; j < C::kCW; ++j) {
               const int m = m0 + col0 + j;
-              if (m < args.M) args.Y[(int64_t)m * args.ldy + n] = __float2half_rn(y[j]);
+              if (m < args.M) {
+                const __half hv = __float2half_rn(y[j]);
+                args.Y[(int64_t)m * args.ldy + n] = hv;
+                for (int i = 0; i < args.npeer; ++i) args.Ypeer[i][(int64_t)m * args.ldy + n] = hv;  // f1
+              }
             }
             if (threadIdx.x == 32 * C::kEpiWarp0) args.ws_counter[t] = 0;
           }

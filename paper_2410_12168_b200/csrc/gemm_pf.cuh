@@ -231,7 +231,7 @@ template <bool kGroupK, bool kAccOut>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
     w4ax_gemm_pf_kernel(const __grid_constant__ CUtensorMap tmXe, const __grid_constant__ CUtensorMap tmX8,
                         const __grid_constant__ CUtensorMap tmY, const __grid_constant__ BlockMap map, GemmArgs args,
-                        PfSched sched) {
+                        PfSched sched, const __grid_constant__ YPeerMaps ypeers) {
   using C = PfCfg;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
@@ -597,7 +597,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&tmY, ybox, 2 * (n0 + kWC * kw + 32 * h), m0 + 128 * (int)crank + 32 * q);
+              const int yx = 2 * (n0 + kWC * kw + 32 * h), yy = m0 + 128 * (int)crank + 32 * q;
+              tma_store_2d(&tmY, ybox, yx, yy);
+              // f1: the same box into every peer's copy of the output (NVLink
+              // P2P stores from the TMA engine; "all-gather fused into
+              // the epilogue", one sync before the write-back is consumed)
+              for (int i = 0; i < ypeers.n; ++i) tma_store_2d(&ypeers.m[i], ybox, yx, yy);
               bulk_commit_group();
             }
           }

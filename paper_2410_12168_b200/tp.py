@@ -128,3 +128,52 @@ def row_parallel_reduce(y_partial: torch.Tensor, group=None, scatter: bool = Tru
     dist.reduce_scatter_tensor(out, buf, group=group)
     rank = dist.get_rank(group)
     return out[: max(0, min(per, M - rank * per))]
+
+
+# ------------------------- all-gather fused into the GEMM ----
+class FusedAllGatherOutput:
+    """The full-width output [M x P*per] fp16 of an N-sharded layer in
+    symmetric memory (torch.distributed._symmetric_memory: one allocation per
+    rank, every peer's copy mapped into this process over NVLink P2P).  Each
+    rank's comet_w4ax_linear_allgather writes its shard's Y tiles straight into
+    ALL ranks' copies from the GEMM epilogue (the all-gather fused
+    into the epilogue); barrier() is the single cross-rank sync after which
+    every rank's copy holds the whole Y.  No NCCL call and no reassembly
+    kernel on this path."""
+
+    def __init__(self, M: int, per: int, device, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.per = per
+        self.buf = symm_mem.empty((M, self.world * per), dtype=torch.float16, device=device)
+        grp = group if group is not None else dist.group.WORLD
+        self.handle = symm_mem.rendezvous(self.buf, grp)
+        self.ptrs = [int(self.handle.buffer_ptrs[r]) for r in range(self.world)]
+
+    def dests(self):
+        """this rank's copy first, then the peers' (the C ABI's Ys[])"""
+        return [self.ptrs[self.rank]] + [self.ptrs[r] for r in range(self.world) if r != self.rank]
+
+    @property
+    def ldy(self):
+        return self.world * self.per
+
+    @property
+    def col0(self):
+        return self.rank * self.per
+
+    def barrier(self):
+        self.handle.barrier()
+
+    def full(self, N: int) -> torch.Tensor:
+        return self.buf[:, :N]
+
+
+def fused_linear_allgather(comet_mod, X, bits, Wq_shard, Sw_shard, out: FusedAllGatherOutput, perm=None,
+                           group_size: int = 128, scratch=None, stream=None):
+    """One N-sharded layer: quantize + GEMM whose epilogue stores into every
+    rank's copy of `out`, then the one barrier."""
+    comet_mod.comet_w4ax_linear_allgather(X, bits, Wq_shard, Sw_shard, out.dests(), out.ldy, out.col0, perm=perm,
+                                          group=group_size, scratch=scratch, stream=stream)
+    out.barrier()
