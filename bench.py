@@ -14,8 +14,11 @@ synthetic inputs (paper_2410_12168_b200.synth).  One step =
 one pass of the hot path over every layer through the whole-layer entry
 comet_w4ax_linear (device X and Y: a1+a2 quantize, a3..a8 GEMM; at prefill
 sizes its quantizer writes the GEMM's e4m3 token operand directly); with N > 1 GPUs the weights are N-sharded
-(tensor parallel), X is replicated, and each layer's Y shards are all-gathered
-(NCCL) and reassembled into Y [M x N] by comet_gather_shards inside the step.
+(tensor parallel), X is replicated, and each rank's GEMM epilogue stores its
+Y tiles into every rank's full [M x N] output in symmetric memory
+(comet_w4ax_linear_allgather: the all-gather fused into the epilogue, f1), one
+barrier per layer; --tp-exchange nccl (or no symmetric memory) all-gathers the
+shards with NCCL and reassembles them with comet_gather_shards instead.
 Weights are packed once before timing (a0 is offline); its time is
 reported as pack_weight_ms.
 
@@ -302,8 +305,21 @@ def run_comet(args, cfg, config_name):
         del p
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
-    # f1: for N > 1, row chunks pipeline GEMM and all-gather
-    chunks = args.overlap_chunks if args.overlap_chunks > 0 else (4 if (world > 1 and M >= 1024) else 1)
+    # f1: for N > 1 the GEMM epilogue stores every Y tile into all ranks' copies of the
+    # full output (symmetric memory, NVLink P2P) and one barrier ends the layer; fallback (no
+    # symmetric memory): row chunks pipelining GEMM and an NCCL all-gather
+    exchange = "single"
+    if world > 1:
+        exchange = "nccl"
+        if args.tp_exchange == "fused":
+            try:
+                for L in layers:
+                    L["fused_out"] = tp.FusedAllGatherOutput(M, L["per"], dev)
+                exchange = "fused"
+            except Exception as e:  # noqa: BLE001 -- no P2P / symmetric memory on this node
+                print(f"[bench] fused all-gather unavailable ({type(e).__name__}: {e}); NCCL all-gather",
+                      file=sys.stderr)
+    chunks = args.overlap_chunks if args.overlap_chunks > 0 else (4 if (exchange == "nccl" and M >= 1024) else 1)
     if world > 1 and chunks > 1:
         for L in layers:
             L["cplanes"] = {b: comet.alloc_act_planes(b[1] - b[0], L["K"], L["bits"], dev)
@@ -312,6 +328,10 @@ def run_comet(args, cfg, config_name):
     def layer_fwd(L, gname, timed=False):
         Wq, Sw = L["packed"][gname]
         grp = group_of(gname, L["K"])
+        if exchange == "fused" and not timed:
+            tp.fused_linear_allgather(comet, L["X"], L["bits"], Wq, Sw, L["fused_out"], perm=L["perm"],
+                                      group_size=grp, scratch=L["scratch"])
+            return
         if world > 1 and chunks > 1:
             def gemm_rows(m0, m1, out):
                 Xq8, Xq4, Sx = comet.comet_quantize_act(L["X"][m0:m1], L["bits"], L["perm"], out=L["cplanes"][(m0, m1)])
@@ -338,7 +358,7 @@ def run_comet(args, cfg, config_name):
             L["qev"].append((qa, qb))
             L["ev"].append((qb, gb))
             L["lev"].append((la, lb))
-        if world > 1:
+        if world > 1 and exchange == "nccl":
             tp.all_gather_y(L["Y"], out=L["Yall"])
             comet.comet_gather_shards(L["Yall"], L["N"], out=L["Yfull"])
 
@@ -486,8 +506,11 @@ def run_comet(args, cfg, config_name):
            "data": "synthetic (seeded; X~N(0,1) + planted outlier channels, W~N(0,1/K)); random-init weights",
            "config": {"workload": cfg["workload"], "M": M, "layers": cfg["layers"], "weight_scales": wsname,
                       "weights": "INT4 packed",
-                      "parallelism": (f"tp{world} (N-sharded; NCCL all-gather of Y + comet_gather_shards to [M x N]"
-                                      + (f", {chunks} row chunks pipelining GEMM and all-gather)" if chunks > 1 else ")")
+                      "parallelism": ((f"tp{world} (N-sharded; the GEMM epilogue stores every Y tile into all "
+                                       f"ranks' [M x N] copies in symmetric memory over NVLink, one barrier per layer)")
+                                      if exchange == "fused" else
+                                      (f"tp{world} (N-sharded; NCCL all-gather of Y + comet_gather_shards to [M x N]"
+                                       + (f", {chunks} row chunks pipelining GEMM and all-gather)" if chunks > 1 else ")"))
                                       if world > 1 else "single GPU"),
                       "timing": ("CUDA graph replay per step" if use_graph else "stream launches per step")
                                 + f", median of {args.steps} event-timed steps",
@@ -535,6 +558,8 @@ def main():
                          "the paper's setting, P:L396) or 128-channel groups (SURVEY 8(d)); the other one is timed too")
     ap.add_argument("--no-alt-group", action="store_true", help="skip timing the other weight-scale granularity")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--tp-exchange", default="fused", choices=["fused", "nccl"],
+                    help="N > 1: all-gather fused into the GEMM epilogue (symmetric memory) or NCCL all-gather")
     ap.add_argument("--overlap-chunks", type=int, default=0,
                     help="N > 1: row chunks pipelining GEMM and all-gather (0: auto = 4 for M >= 1024, 1: serial)")
     args = ap.parse_args()
