@@ -234,3 +234,13 @@ def test_row_parallel_shards_through_the_cuda_path():
         total += ref
         bound += np.maximum(2.0 ** -10 * np.abs(ref), 1e-3)
     assert np.all(np.abs(gpu - total) <= bound)
+
+
+def test_fused_allgather_destination_order():
+    """f1 host logic: this rank's copy first, then the peers' (the C ABI's
+    Ys[]), the shard's column offset and the full row stride."""
+    o = tp.FusedAllGatherOutput.__new__(tp.FusedAllGatherOutput)
+    o.world, o.rank, o.per = 4, 2, 384
+    o.ptrs = [1000, 2000, 3000, 4000]
+    assert o.dests() == [3000, 1000, 2000, 4000]
+    assert o.col0 == 768 and o.ldy == 1536
