@@ -12,4 +12,3 @@ timeout -s KILL 300 python bench.py --impl reference --steps 3 --warmup 3 > gpur
 timeout -s KILL 600 python tools/quant_sweep.py > gpurun_out/quant_sweep_r2.txt 2>&1; echo qs_rc=$?
 timeout -s KILL 600 python tools/quant_sweep.py '[[8192, 4096, 3], [8192, 14336, 11], [16384, 8192, 6], [8192, 28672, 22]]' fmpq >> gpurun_out/quant_sweep_r2.txt 2>&1; echo qsf_rc=$?
 bash tools/profile_round.sh
-bash tools/gpu_sanitize.sh

@@ -71,7 +71,7 @@ def main(rnd):
           "CUDA-event numbers; compare shares and counters, not absolutes).", ""]
     traffic = {}
     for tag, rep in [("prefill GEMM (LLaMA-3-8B gate_up 28672x4096 and down 4096x14336, M=8192, per-channel weight scales)", "prof_gemm_full"),
-                     ("quantize_act (LLaMA-3-8B, M=8192; layers 2 and 3)", "prof_quant_full"),
+                     ("quantize_act: quantize_lane_kernel (LLaMA-3-8B, M=8192, FMPQ permutation; layers 2 and 3)", "prof_quant_full"),
                      ("decode GEMM (LLaMA-3-70B, M=16; layers 2 and 3)", "prof_decode_full")]:
         path = os.path.join(OUT, rep + ".ncu-rep")
         if not os.path.exists(path):
