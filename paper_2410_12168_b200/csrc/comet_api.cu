@@ -1089,6 +1089,12 @@ comet_status comet_quantize_kv(const void* KV, int64_t ld, int32_t T, int32_t C,
   if ((reinterpret_cast<uintptr_t>(KV) & 3) || (reinterpret_cast<uintptr_t>(scale) & 3)) return COMET_ERR_ALIGNMENT;
   comet_status ds = device_check(nullptr);
   if (ds != COMET_OK) return ds;
+  if (C % 8 == 0 && ld % 8 == 0 && !(reinterpret_cast<uintptr_t>(KV) & 15) && !(reinterpret_cast<uintptr_t>(Q) & 3)) {
+    const dim3 gv((unsigned)((C + 63) / 64), (unsigned)((T + group - 1) / group));
+    kv4_quantize_v_kernel<<<gv, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const __half*>(KV), ld, T, C, group, reinterpret_cast<uint8_t*>(Q), scale, zp);
+    return check_launch();
+  }
   const dim3 grid((unsigned)((C / 2 + 63) / 64), (unsigned)((T + group - 1) / group));
   kv4_quantize_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __half*>(KV), ld, T, C, group, reinterpret_cast<uint8_t*>(Q), scale, zp);
@@ -1104,6 +1110,13 @@ comet_status comet_dequantize_kv(const void* Q, const float* scale, const uint8_
   if ((reinterpret_cast<uintptr_t>(out) & 3) || (reinterpret_cast<uintptr_t>(scale) & 3)) return COMET_ERR_ALIGNMENT;
   comet_status ds = device_check(nullptr);
   if (ds != COMET_OK) return ds;
+  if (C % 16 == 0 && ldo % 8 == 0 && !(reinterpret_cast<uintptr_t>(out) & 15) && !(reinterpret_cast<uintptr_t>(Q) & 7) &&
+      !(reinterpret_cast<uintptr_t>(scale) & 15) && !(reinterpret_cast<uintptr_t>(zp) & 15)) {
+    const int64_t n = (int64_t)T * (C / 16);
+    kv4_dequantize_v_kernel<<<(unsigned)((n + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const uint8_t*>(Q), scale, zp, T, C, group, reinterpret_cast<__half*>(out), ldo);
+    return check_launch();
+  }
   const int64_t units = (int64_t)T * (C / 2);
   kv4_dequantize_kernel<<<(unsigned)((units + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const uint8_t*>(Q), scale, zp, T, C, group, reinterpret_cast<__half*>(out), ldo);

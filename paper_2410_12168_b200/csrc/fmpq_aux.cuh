@@ -157,6 +157,115 @@ __global__ void __launch_bounds__(256) kv4_dequantize_kernel(const uint8_t* __re
   }
 }
 
+// Vectorised KV4 quantization (C % 8 == 0, 16-byte aligned rows): CTA = one
+// token group x 64 channels (8 channel octets x 32 token lanes: 4 rows of
+// 128 B per warp load).  Pass 1: 16-byte loads, per-channel min/max over the
+// group reduced across the token lanes in shared memory; one thread per
+// channel derives (scale, zp) as kv_params; pass 2 re-reads the group
+// (L1/L2-resident) and writes one 4-byte packed word (8 channels) per token.
+// Same arithmetic as kv4_quantize_kernel.
+__global__ void __launch_bounds__(256) kv4_quantize_v_kernel(const __half* __restrict__ KV, int64_t ld, int T, int C,
+                                                             int G, uint8_t* __restrict__ Q, float* __restrict__ scale,
+                                                             uint8_t* __restrict__ zp) {
+  __shared__ float red[2][32][65];  // [min, max][token lane][channel]
+  __shared__ float ps[64];
+  __shared__ int pz[64];
+  const int ol = threadIdx.x & 7, tl = threadIdx.x >> 3;
+  const int c0 = blockIdx.x * 64 + ol * 8;
+  const bool live = c0 < C;
+  const int g = blockIdx.y;
+  const int t0 = g * G, t1 = min(T, t0 + G);
+  float mn[8], mx[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) mn[j] = INFINITY, mx[j] = -INFINITY;
+  if (live) {
+    for (int t = t0 + tl; t < t1; t += 32) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(KV + (int64_t)t * ld + c0));
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float x0 = half_bits_to_float(w[j] & 0xFFFF), x1 = half_bits_to_float(w[j] >> 16);
+        mn[2 * j] = fminf(mn[2 * j], x0), mx[2 * j] = fmaxf(mx[2 * j], x0);
+        mn[2 * j + 1] = fminf(mn[2 * j + 1], x1), mx[2 * j + 1] = fmaxf(mx[2 * j + 1], x1);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) red[0][tl][ol * 8 + j] = mn[j], red[1][tl][ol * 8 + j] = mx[j];
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int ch = threadIdx.x, c = blockIdx.x * 64 + ch;
+    float a = red[0][0][ch], b = red[1][0][ch];
+    for (int r = 1; r < 32; ++r) a = fminf(a, red[0][r][ch]), b = fmaxf(b, red[1][r][ch]);
+    float sc = 1.0f;
+    int z = 0;
+    if (c < C) {
+      kv_params(a, b, sc, z);
+      scale[(int64_t)g * C + c] = sc;
+      zp[(int64_t)g * C + c] = (uint8_t)z;
+    }
+    ps[ch] = sc;
+    pz[ch] = z;
+  }
+  __syncthreads();
+  if (!live) return;
+  float sv[8];
+  int zv[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) sv[j] = ps[ol * 8 + j], zv[j] = pz[ol * 8 + j];
+  for (int t = t0 + tl; t < t1; t += 32) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(KV + (int64_t)t * ld + c0));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t packed = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float x0 = half_bits_to_float(w[j] & 0xFFFF), x1 = half_bits_to_float(w[j] >> 16);
+      const int q0 = min(15, max(0, round_half_away(__fdiv_rn(x0, sv[2 * j])) + zv[2 * j]));
+      const int q1 = min(15, max(0, round_half_away(__fdiv_rn(x1, sv[2 * j + 1])) + zv[2 * j + 1]));
+      packed |= (uint32_t)(q0 | (q1 << 4)) << (8 * j);
+    }
+    *reinterpret_cast<uint32_t*>(Q + (int64_t)t * (C / 2) + c0 / 2) = packed;
+  }
+}
+
+// Vectorised KV4 dequantization (C % 16 == 0, 16-byte aligned output rows):
+// thread = one token x 16 channels: one 8-byte load of the packed row, the
+// channels' zero points (16 B) and scales (64 B, L1-resident across the
+// group's tokens), two 16-byte stores.  n - zp is formed exactly as a float
+// difference of 2^23 + n and 2^23 + zp (no int -> float conversion), then
+// fp16_rn(fp32(n - zp) * scale) as kv4_dequantize_kernel.
+__global__ void __launch_bounds__(256) kv4_dequantize_v_kernel(const uint8_t* __restrict__ Q,
+                                                               const float* __restrict__ scale,
+                                                               const uint8_t* __restrict__ zp, int T, int C, int G,
+                                                               __half* __restrict__ out, int64_t ldo) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nc = C / 16;
+  if (i >= (int64_t)T * nc) return;
+  const int t = (int)(i / nc), c0 = (int)(i % nc) * 16;
+  const int64_t prow = (int64_t)(t / G) * C + c0;
+  const uint2 qv = __ldg(reinterpret_cast<const uint2*>(Q + (int64_t)t * (C / 2) + c0 / 2));
+  const uint4 zq = __ldg(reinterpret_cast<const uint4*>(zp + prow));
+  const float4* sp = reinterpret_cast<const float4*>(scale + prow);
+  const float4 s4[4] = {__ldg(sp), __ldg(sp + 1), __ldg(sp + 2), __ldg(sp + 3)};
+  const float sc[16] = {s4[0].x, s4[0].y, s4[0].z, s4[0].w, s4[1].x, s4[1].y, s4[1].z, s4[1].w,
+                        s4[2].x, s4[2].y, s4[2].z, s4[2].w, s4[3].x, s4[3].y, s4[3].z, s4[3].w};
+  const uint32_t qw[2] = {qv.x, qv.y}, zw[4] = {zq.x, zq.y, zq.z, zq.w};
+  uint32_t o[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {  // packed byte j = channels 2j (low nibble), 2j + 1 (high)
+    const uint32_t b = (qw[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+    const uint32_t z0 = (zw[(2 * j) >> 2] >> (8 * ((2 * j) & 3))) & 0xFFu;
+    const uint32_t z1 = (zw[(2 * j + 1) >> 2] >> (8 * ((2 * j + 1) & 3))) & 0xFFu;
+    const float d0 = __fsub_rn(__uint_as_float(0x4B000000u | (b & 0xFu)), __uint_as_float(0x4B000000u | z0));
+    const float d1 = __fsub_rn(__uint_as_float(0x4B000000u | (b >> 4)), __uint_as_float(0x4B000000u | z1));
+    const __half2 h = __floats2half2_rn(__fmul_rn(d0, sc[2 * j]), __fmul_rn(d1, sc[2 * j + 1]));
+    o[j] = *reinterpret_cast<const uint32_t*>(&h);
+  }
+  uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)t * ldo + c0);
+  dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+  dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
 // f4: static per-block activation scales:
 // scale[b] = fp32(pool_b / qmax_b), pool_b = max of the calibration maxabs over
 // the block's channels on the permuted axis, 1 if pool_b == 0.  CTA = block.

@@ -259,8 +259,12 @@ def test_calibrated_map_drives_the_w4ax_path():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("T,C,G", [(1, 64, 128), (16, 128, 16), (129, 128, 64), (300, 256, 128)])
+@pytest.mark.parametrize("T,C,G", [(1, 64, 128), (16, 128, 16), (129, 128, 64), (300, 256, 128),
+                                   (1000, 1024, 100), (37, 8, 5), (50, 70, 16), (2048, 4096, 128)])
 def test_kv4_bit_exact(T, C, G):
+    """vectorised kernels (C % 8 / C % 16 == 0: groups not dividing T, G not a
+    multiple of the 8 token lanes, channel tiles of 256 past C) and the
+    scalar fallbacks (C = 70; C = 8 dequantizes through the fallback)"""
     import torch
     from paper_2410_12168_b200 import comet
     rng = np.random.default_rng(T * C + G)

@@ -54,6 +54,16 @@ def main():
     t = timed(lambda: comet.comet_dequantize_kv(Q, s, z, 128))
     byts = KV.numel() // 2 + KV.numel() * 2 + 8192 // 128 * 1024 * 5
     out.append({"kernel": "kv4_dequantize", "shape": [8192, 1024, 128], "us": t * 1e6, "GBs": byts / t / 1e9})
+    # the same at a size where the fixed launch cost (~5 us per event-timed kernel) stops mattering:
+    # 131072 tokens (a 32k context x 4 sequences) x 1024
+    KVb = torch.randn(131072, 1024, device="cuda").half()
+    t = timed(lambda: comet.comet_quantize_kv(KVb, 128))
+    byts = KVb.numel() * 2 + KVb.numel() // 2 + 131072 // 128 * 1024 * 5
+    out.append({"kernel": "kv4_quantize", "shape": [131072, 1024, 128], "us": t * 1e6, "GBs": byts / t / 1e9})
+    Qb, sb, zb = comet.comet_quantize_kv(KVb, 128)
+    t = timed(lambda: comet.comet_dequantize_kv(Qb, sb, zb, 128))
+    out.append({"kernel": "kv4_dequantize", "shape": [131072, 1024, 128], "us": t * 1e6, "GBs": byts / t / 1e9})
+    del KVb, Qb, sb, zb
     # f4: static-scale activation quantize vs the dynamic one, M=K=4096, 3/32 INT8 blocks
     M, K = 4096, 4096
     bits = np.full(K // 128, 4, np.uint8)
