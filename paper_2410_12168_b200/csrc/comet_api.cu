@@ -31,6 +31,9 @@ std::atomic<int64_t> g_launches{0};
 std::atomic<int> g_pf_clusters{0};
 // tools only (comet_debug_set_pf_group): token tiles per raster group, 0 = by L2 budget
 std::atomic<int> g_pf_group{0};
+// tools only (comet_debug_set_prefill_min_m): M above which the prefill kernel runs
+// (0 = the product rule)
+std::atomic<int> g_pf_min_m{0};
 
 comet_status cuda_fail(cudaError_t e) {
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
@@ -183,9 +186,28 @@ struct Plan {
 constexpr int64_t kCounterBytes = 64 * 1024;
 int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
 
-Plan make_plan(int M, int N, int K, int num_sms) {
+// Kernel choice by M (per_channel: 1 = weight scales per output channel, 0 =
+// group 128, -1 = unknown).  The prefill kernel above 128 tokens; with
+// per-channel scales already above 64: there one half-empty 256-token tile of
+// the CTA-pair kernel beats the decode kernel's BN = 128 tiles on every
+// measured shape (70B gate_up 171 vs 189-194 us, 8B gate_up 60 vs 83-85 us, 8B
+// down 66.5 vs 67-71 us at M = 80..128; tools/mband_sweep.py,
+// profiles/mband_sweep_r2.txt), while with group-128 scales the decode kernel
+// wins on two of the three shapes.  Unknown (the workspace-size query): the
+// plan of the two with the larger workspace, so one buffer serves both.
+Plan make_plan_for(int M, int N, int K, int num_sms, bool two_sm);
+Plan make_plan(int M, int N, int K, int num_sms, int per_channel = -1) {
+  const int pf_min = g_pf_min_m.load(std::memory_order_relaxed);
+  if (pf_min > 0) return make_plan_for(M, N, K, num_sms, M > pf_min);
+  if (M > 128 || M <= 64) return make_plan_for(M, N, K, num_sms, M > 128);
+  if (per_channel >= 0) return make_plan_for(M, N, K, num_sms, per_channel == 1);
+  const Plan a = make_plan_for(M, N, K, num_sms, true), b = make_plan_for(M, N, K, num_sms, false);
+  if (a.ws_bytes < 0 || b.ws_bytes < 0) return a.ws_bytes < 0 ? a : b;
+  return a.ws_bytes >= b.ws_bytes ? a : b;
+}
+Plan make_plan_for(int M, int N, int K, int num_sms, bool two_sm) {
   Plan p;
-  p.two_sm = M > 128;
+  p.two_sm = two_sm;
   p.splits = 1;
   if (p.two_sm) {
     p.bn = 128;  // token rows per CTA (TMA box height)
@@ -331,7 +353,7 @@ comet_status gemm_common(const int8_t* Xq8, const void* Xq4, const float* Sx, in
   int num_sms = 148;
   comet_status ds = device_check(&num_sms);
   if (ds != COMET_OK) return ds;
-  Plan p = make_plan(M, N, K, num_sms);
+  Plan p = make_plan(M, N, K, num_sms, group == K ? 1 : 0);
   if (p.ws_bytes < 0) return COMET_ERR_SHAPE;
   if (p.ws_bytes > 0 && (ws == nullptr || (int64_t)ws_bytes < p.ws_bytes)) return COMET_ERR_WORKSPACE;
 
@@ -648,7 +670,7 @@ static comet_status linear_impl(const void* X, int64_t ldx, int32_t M, int32_t K
   if (group != 128 && group != K) return COMET_ERR_SHAPE;
   if (K > 65536) return COMET_ERR_SHAPE;
   if (!aligned16(Wq) || !aligned16(Sw) || (perm && !aligned16(perm)) || !aligned16(scratch)) return COMET_ERR_ALIGNMENT;
-  if (make_plan(M, N, K, 148).ws_bytes < 0) return COMET_ERR_SHAPE;
+  if (make_plan(M, N, K, 148, group == K ? 1 : 0).ws_bytes < 0) return COMET_ERR_SHAPE;
   comet_status ds = device_check(nullptr);
   if (ds != COMET_OK) return ds;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -689,7 +711,7 @@ static comet_status linear_impl(const void* X, int64_t ldx, int32_t M, int32_t K
   auto layer = [&](const void* Xd, int64_t ldxd, int32_t mc, void* Yd, int64_t ldyd) -> comet_status {
     const int64_t ldsx = comet_act_ldsx(mc);
     const int64_t wsb = comet_w4ax_gemm_workspace_bytes(mc, N, K);
-    if (make_plan(mc, N, K, 148).two_sm && (int64_t)kQNBuf * K * 2 <= 200 * 1024) {
+    if (make_plan(mc, N, K, 148, group == K ? 1 : 0).two_sm && (int64_t)kQNBuf * K * 2 <= 200 * 1024) {
       // prefill: the quantizer writes the GEMM's e4m3 token operand and its
       // corrections straight into the workspace (no packed INT4 plane, no token
       // preparation kernel); identical results to the two-call path
@@ -1157,6 +1179,13 @@ int comet_debug_set_pf_clusters(int n) {
 // L2-budget rule).  Results are identical.
 int comet_debug_set_pf_group(int n) {
   g_pf_group.store(n < 0 ? 0 : n);
+  return 0;
+}
+// Kernel-choice sweep: M above which the CTA-pair prefill kernel runs instead
+// of the decode kernel (0 = the product rule).  Results agree within the Y
+// tolerance (the INT32 accumulators are identical).
+int comet_debug_set_prefill_min_m(int m) {
+  g_pf_min_m.store(m < 0 ? 0 : m);
   return 0;
 }
 

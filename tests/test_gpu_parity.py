@@ -455,3 +455,25 @@ def test_power_of_two_scales_bit_exact_prefill(M, group):
     r = oracle.w4ax_gemm(Xq8, Xq4, Sx, p["bits"], Wq, Sw, group=group, rows=rows, want_y64=True)
     assert np.array_equal(r["y64"], p["X"][rows].astype(np.float64) @ p["W"].astype(np.float64).T)
     assert np.array_equal(g["Y"][rows].view(np.uint16), r["y"].view(np.uint16))
+
+
+@pytest.mark.parametrize("M", [65, 100, 128])
+def test_kernel_choice_band_both_kernels(M):
+    """64 < M <= 128 with per-channel weight scales runs the CTA-pair prefill
+    kernel (faster there, profiles/mband_sweep_r2.txt); the decode kernel's
+    BN = 128 per-channel specialisation stays checked by forcing it through
+    the tools-only comet_debug_set_prefill_min_m hook."""
+    import ctypes
+    L = comet.lib()
+    L.comet_debug_set_prefill_min_m.argtypes = [ctypes.c_int]
+    p = synth.make_problem(M, 640, 2048, n8=2, seed=900 + M, mask="scattered")
+    o = oracle_path(p, 2048, want_acc=True)
+    try:
+        for force in (0, 1000):
+            L.comet_debug_set_prefill_min_m(force)
+            g = gpu_path(p, 2048, want_acc=True)
+            assert_planes_equal(g, o)
+            assert np.array_equal(g["Acc"], o["acc"])
+            assert_y_close(g["Y"], o["y"], o["y64"])
+    finally:
+        L.comet_debug_set_prefill_min_m(0)
