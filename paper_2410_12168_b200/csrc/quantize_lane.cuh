@@ -166,8 +166,20 @@ DEVI void lane_gather(uint32_t (&w)[kLaneSub / 2], uint32_t ubase, uint32_t tab_
   }
 }
 
+// __launch_bounds__ thread counts, i.e. the register caps (the launches use
+// <= kLaneMaxThreads + 32 threads either way): the packed-plane variant is
+// 5-11% faster capped at 80 registers (bound 672: 8192 x 14336 FMPQ 114 ->
+// 102 us, 8192 x 28672 217 -> 203 us, 8192 x 4096 unchanged; a bound of 768,
+// also 80 registers, measured slower: the schedule differs), the e4m3
+// variant of comet_w4ax_linear measured neutral and keeps 96
+#ifndef COMET_LANE_LB_PK
+#define COMET_LANE_LB_PK 672
+#endif
+#ifndef COMET_LANE_LB_E4
+#define COMET_LANE_LB_E4 (kLaneMaxThreads + 32)
+#endif
 template <bool kE4, bool kBf16, bool kPerm>
-__global__ void __launch_bounds__(kLaneMaxThreads + 32, 1)
+__global__ void __launch_bounds__(kE4 ? COMET_LANE_LB_E4 : COMET_LANE_LB_PK, 1)
     quantize_lane_kernel(const __half* __restrict__ X, int64_t ldx, int M, int nb, int64_t ldsx,
                          const int32_t* __restrict__ perm, const __grid_constant__ BlockMap map,
                          int8_t* __restrict__ Xq8, int64_t ld8, uint8_t* __restrict__ Xo4, int64_t ld4,
