@@ -170,13 +170,14 @@ DEVI void lane_gather(uint32_t (&w)[kLaneSub / 2], uint32_t ubase, uint32_t tab_
 // <= kLaneMaxThreads + 32 threads either way): the packed-plane variant is
 // 5-11% faster capped at 80 registers (bound 672: 8192 x 14336 FMPQ 114 ->
 // 102 us, 8192 x 28672 217 -> 203 us, 8192 x 4096 unchanged; a bound of 768,
-// also 80 registers, measured slower: the schedule differs), the e4m3
-// variant of comet_w4ax_linear measured neutral and keeps 96
+// also 80 registers, measured slower: the schedule differs); the e4m3
+// variant of comet_w4ax_linear at 80 registers (bound 704) saves ~4 us on
+// the 8B down projection and is neutral on the K = 4096 layers
 #ifndef COMET_LANE_LB_PK
 #define COMET_LANE_LB_PK 672
 #endif
 #ifndef COMET_LANE_LB_E4
-#define COMET_LANE_LB_E4 (kLaneMaxThreads + 32)
+#define COMET_LANE_LB_E4 704
 #endif
 template <bool kE4, bool kBf16, bool kPerm>
 __global__ void __launch_bounds__(kE4 ? COMET_LANE_LB_E4 : COMET_LANE_LB_PK, 1)
