@@ -11,4 +11,6 @@ timeout -s KILL 900 python bench.py --config llama2-7b --no-cpu-baseline > gpuru
 timeout -s KILL 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_r2_ref.json 2> gpurun_out/bench_r2_ref.err; echo ref_rc=$?
 timeout -s KILL 600 python tools/quant_sweep.py > gpurun_out/quant_sweep_r2.txt 2>&1; echo qs_rc=$?
 timeout -s KILL 600 python tools/quant_sweep.py '[[8192, 4096, 3], [8192, 14336, 11], [16384, 8192, 6], [8192, 28672, 22]]' fmpq >> gpurun_out/quant_sweep_r2.txt 2>&1; echo qsf_rc=$?
+timeout -s KILL 600 python tools/aux_bench.py > gpurun_out/aux_bench_r2.txt 2>&1; echo aux_rc=$?
+timeout -s KILL 900 python tools/m_sweep.py > gpurun_out/m_sweep_r2b.txt 2>&1; echo msw_rc=$?
 bash tools/profile_round.sh
