@@ -145,7 +145,10 @@ DEVI void tmem_ld_n<8>(uint32_t taddr, uint32_t (&r)[8]) {
 DEVI void epi_sync(int nthreads) { asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory"); }
 
 template <int BN, bool kGroupK, bool kAccOut>
-__global__ void __launch_bounds__(DecCfg<BN>::kThreads, 1)
+#ifndef DEC_LB
+#define DEC_LB 0  // 0: DecCfg<BN>::kThreads (tools: a larger bound lowers the register cap)
+#endif
+__global__ void __launch_bounds__(DEC_LB > 0 ? DEC_LB : DecCfg<BN>::kThreads, 1)
     w4ax_gemm_decode_kernel(const __grid_constant__ CUtensorMap tmSx, const __grid_constant__ CUtensorMap tmX4,
                             const __grid_constant__ CUtensorMap tmX8, const __grid_constant__ CUtensorMap tmSw,
                             const __grid_constant__ BlockMap map, GemmArgs args, DecSched sched) {

@@ -228,7 +228,10 @@ __global__ void __launch_bounds__(256) prep_tokens_kernel(const uint8_t* __restr
 // corrections.
 // kAccOut: write per-block INT32 accumulators (debug entry).
 template <bool kGroupK, bool kAccOut>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PfCfg::kThreads, 1)
+#ifndef PF_LB
+#define PF_LB 0  // 0: PfCfg::kThreads (tools: a larger bound lowers the register cap)
+#endif
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PF_LB > 0 ? PF_LB : PfCfg::kThreads, 1)
     w4ax_gemm_pf_kernel(const __grid_constant__ CUtensorMap tmXe, const __grid_constant__ CUtensorMap tmX8,
                         const __grid_constant__ CUtensorMap tmY, const __grid_constant__ BlockMap map, GemmArgs args,
                         PfSched sched, const __grid_constant__ YPeerMaps ypeers) {
