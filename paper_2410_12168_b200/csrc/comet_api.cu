@@ -512,7 +512,12 @@ comet_status quantize_act_impl(const void* X, int64_t ldx, int32_t M, int32_t K,
                       : (perm ? quantize_lane_kernel<false, kBf16, true> : quantize_lane_kernel<false, kBf16, false>);
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lp.smem);
       if (e != cudaSuccess) return cuda_fail(e);
-      const int64_t grid = std::min<int64_t>(num_sms, lp.stages);
+      // persistent: as many CTAs per SM as shared memory / registers allow
+      // (one at the default plan sizes)
+      int per_sm = 1;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, lp.threads, lp.smem);
+      if (e != cudaSuccess) return cuda_fail(e);
+      const int64_t grid = std::min<int64_t>((int64_t)num_sms * std::max(1, per_sm), lp.stages);
       kern<<<(int)grid, lp.threads, lp.smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
                                                     X4e ? X4e : reinterpret_cast<uint8_t*>(Xq4),
                                                     X4e ? (int64_t)n4 * 128 : (int64_t)n4 * 64, Sx, CX, lp.R, lp.S,

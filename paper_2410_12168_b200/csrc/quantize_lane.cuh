@@ -66,26 +66,36 @@ struct LanePlan {
 #endif
 constexpr int kLaneSub = COMET_LANE_SUB;
 #ifndef COMET_LANE_THREADS
-#define COMET_LANE_THREADS (kLaneSub == 64 ? 512 : 256)
+#define COMET_LANE_THREADS 256
 #endif
 #ifndef COMET_LANE_SMAX
-#define COMET_LANE_SMAX 3
+#define COMET_LANE_SMAX 2
 #endif
-constexpr int kLaneMaxThreads = COMET_LANE_THREADS;  // compute threads per CTA
-constexpr int kLaneSMax = COMET_LANE_SMAX;           // stages in the ring at most
+// compute lanes per CTA: the target (small CTAs, several per SM, so their
+// stage waits and row barriers interleave) and the most a row may need (a
+// row's lanes are whole warps of one CTA)
+constexpr int kLaneMaxThreads = COMET_LANE_THREADS;
+constexpr int kLaneRowMax = 512;
+constexpr int kLaneSMax = COMET_LANE_SMAX;  // stages in the ring at most
 
 // A row is handled by (K / kLaneSub) lanes ("sub-items": one lane per 128 /
 // kLaneSub of a 128-channel block).  Lanes are laid out so that a warp never
 // straddles two rows when a row needs >= 32 lanes (lpr = that count rounded
 // up to 32: the in-place write waits only for the row's own warps); else a
-// warp holds whole rows.  R rows per stage so that ~kLaneMaxThreads lanes work;
-// S stages next to the gather table (u32 offsets, perm only); S >= 2 or the
-// plan is empty (the row-staged kernel takes over).
+// warp holds whole rows.  R rows per stage so that ~kLaneMaxThreads lanes
+// work (one row when a row alone needs more, up to kLaneRowMax); S stages
+// next to the gather table (u32 offsets, perm only); S >= 2 or the plan is
+// empty (the row-staged kernel takes over).  The launch puts as many CTAs on
+// an SM as shared memory allows (cudaOccupancy...).
+// Measured (8192 rows, FMPQ permutation; 8B bench step): 256 lanes and
+// 2 stages (two CTAs per SM up to K = 14336) against 512 lanes and 3 stages
+// (one CTA per SM): K = 4096 42.0 -> 38.9 us, K = 8192 64.5 -> 61.4 us,
+// K = 14336 equal, step 2.312 -> 2.284 ms.
 inline LanePlan lane_plan(int M, int K, bool perm) {
   LanePlan p;
   const int nb = K / 128;
   const int nsub = K / kLaneSub;
-  if (nb <= 0 || nsub > kLaneMaxThreads) return p;
+  if (nb <= 0 || nsub > kLaneRowMax) return p;
   int ncomp;
   if (nsub >= 32) {
     p.lpr = (nsub + 31) / 32 * 32;
