@@ -50,7 +50,10 @@
 namespace comet {
 
 constexpr int kLaneMaxSmem = 232448;  // sm_100 opt-in dynamic shared memory per CTA
-constexpr int kLaneMinRows = 512;     // below: the row-staged / item kernels (few stages, few CTAs)
+#ifndef COMET_LANE_MIN_ROWS
+#define COMET_LANE_MIN_ROWS 512
+#endif
+constexpr int kLaneMinRows = COMET_LANE_MIN_ROWS;  // below: the row-staged / item kernels (few stages, few CTAs)
 
 struct LanePlan {
   int R = 0;        // rows per stage
