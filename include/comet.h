@@ -255,6 +255,18 @@ comet_status comet_w4ax_gemm_f16s(const int8_t* Xq8, const void* Xq4, const floa
                                   const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq, const void* Sw16,
                                   int32_t N, int32_t group, void* Y, int64_t ldy, void* workspace,
                                   size_t workspace_bytes, comet_stream_t stream);
+/* BF16 storage (SURVEY 8(f) f4 "FP16/BF16 scale storage"): identical to the
+ * fp16 pair above with s = bf16_rn(fp32(a / 7)) (a == 0 -> 1; bf16 keeps
+ * fp32's exponent range, so no underflow clamp) stored as bf16 bits [K/group
+ * x N]; comet_w4ax_gemm_bf16s takes the workspace of
+ * comet_w4ax_gemm_f16s_workspace_bytes and equals comet_w4ax_gemm on the
+ * fp32 values of the bf16 scales. */
+comet_status comet_pack_weight_bf16s(const void* W, int64_t ldw, int32_t N, int32_t K, const int32_t* perm,
+                                     int32_t group, void* Wq, void* Sw16, comet_stream_t stream);
+comet_status comet_w4ax_gemm_bf16s(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
+                                   const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq, const void* Sw16,
+                                   int32_t N, int32_t group, void* Y, int64_t ldy, void* workspace,
+                                   size_t workspace_bytes, comet_stream_t stream);
 
 /* ---- f3: attention over the KV4 cache ("dequant-in-attention") ----------
  * One decode query per head (§3.2: the KV4 cache feeds the

@@ -288,6 +288,39 @@ def pack_weight_f16s(W: np.ndarray, group: int = BLOCK, perm=None):
     return Wq, Sw
 
 
+# f4, BF16 scale storage: as pack_weight_f16s with s = bf16_rn(fp32(a / 7))
+# (round to nearest even on the fp32 bits; bf16 keeps fp32's exponent range,
+# so a nonzero a never gives s = 0; a == 0 -> 1).  Sw16 [K/group x N] as
+# uint16 bf16 encodings.
+def f32_to_bf16_bits(x) -> np.ndarray:
+    u = np.asarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+
+def pack_weight_bf16s(W: np.ndarray, group: int = BLOCK, perm=None):
+    from . import pack_int4
+
+    W = np.asarray(W, dtype=np.float16)
+    N, K = W.shape
+    order = np.arange(K) if perm is None else np.asarray(perm, dtype=np.int64)
+    Wp = W.astype(np.float32)[:, order]
+    ng = K // group
+    Wq = np.zeros((N, K // 2), np.uint8)
+    Sw = np.zeros((ng, N), np.uint16)
+    for n in range(N):
+        row = np.zeros(K, np.int8)
+        for j in range(ng):
+            g = Wp[n, j * group:(j + 1) * group]
+            a = np.float32(np.max(np.abs(g)))
+            sb = f32_to_bf16_bits(np.float32(1.0) if a == 0 else np.float32(a / np.float32(7.0)))
+            Sw[j, n] = sb
+            sf = bf16_bits_to_f32(sb)
+            for i in range(group):
+                row[j * group + i] = _q_static(g[i], np.float32(sf), 7)
+        Wq[n] = pack_int4(row)
+    return Wq, Sw
+
+
 # f4 variant: bf16 activations.  A bf16 value's bits shifted left by 16 are
 # its fp32 encoding (exact); from there the quantization is O3 (the C
 # oracle's oracle_quantize_block, via oracle.quantize_block) on the permuted

@@ -28,6 +28,7 @@ EXPORTS = ["comet_act_plane8_bytes", "comet_act_plane4_bytes", "comet_act_ldsx",
            "comet_quantize_act_bf16", "comet_gather_shards", "comet_w4ax_gemm_allgather",
            "comet_w4ax_linear_allgather", "comet_attention_kv4",
            "comet_pack_weight_f16s", "comet_w4ax_gemm_f16s", "comet_w4ax_gemm_f16s_workspace_bytes",
+           "comet_pack_weight_bf16s", "comet_w4ax_gemm_bf16s",
            "comet_attention_kv4_workspace_bytes",
            "comet_status_str", "comet_last_cuda_error",
            "comet_launch_count"]
@@ -88,6 +89,10 @@ def lib():
         L.comet_w4ax_gemm_f16s_workspace_bytes.restype = i64
         L.comet_w4ax_gemm_f16s.argtypes = [P, P, P, i64, P, i32, i32, P, P, i32, i32, P, i64, P, sz, P]
         L.comet_w4ax_gemm_f16s.restype = ctypes.c_int
+        L.comet_pack_weight_bf16s.argtypes = [P, i64, i32, i32, P, i32, P, P, P]
+        L.comet_pack_weight_bf16s.restype = ctypes.c_int
+        L.comet_w4ax_gemm_bf16s.argtypes = [P, P, P, i64, P, i32, i32, P, P, i32, i32, P, i64, P, sz, P]
+        L.comet_w4ax_gemm_bf16s.restype = ctypes.c_int
         L.comet_attention_kv4_workspace_bytes.argtypes = [i32, i32]
         L.comet_attention_kv4_workspace_bytes.restype = i64
         L.comet_attention_kv4.argtypes = [P, P, P, P, P, P, P, i32, i32, i32, i32, ctypes.c_float, P, P, sz, P]
@@ -325,19 +330,31 @@ def comet_w4ax_gemm(Xq8, Xq4, Sx, bits, Wq, Sw, group: int = BLOCK, out: Optiona
     return Y
 
 
-def comet_pack_weight_f16s(W: torch.Tensor, perm: Optional[torch.Tensor] = None, group: int = BLOCK, stream=None):
-    """f4: as comet_pack_weight, with fp16 scales Sw16 [K/group x N] (the quantization scale)."""
+def comet_pack_weight_f16s(W: torch.Tensor, perm: Optional[torch.Tensor] = None, group: int = BLOCK, stream=None,
+                           bf16: bool = False):
+    """f4: as comet_pack_weight, with fp16 (bf16=True: bf16) scales Sw16 [K/group x N] (the quantization scale)."""
     assert W.is_cuda and W.dtype == torch.float16 and W.dim() == 2 and W.stride(1) == 1
     N, K = W.shape
     Wq = torch.empty((N, K // 2), dtype=torch.uint8, device=W.device)
-    Sw = torch.empty((K // group, N), dtype=torch.float16, device=W.device)
-    st = lib().comet_pack_weight_f16s(_ptr(W), W.stride(0), N, K, _ptr(perm), group, _ptr(Wq), _ptr(Sw), _stream(stream))
-    _check("comet_pack_weight_f16s", st)
+    Sw = torch.empty((K // group, N), dtype=torch.bfloat16 if bf16 else torch.float16, device=W.device)
+    fn = "comet_pack_weight_bf16s" if bf16 else "comet_pack_weight_f16s"
+    st = getattr(lib(), fn)(_ptr(W), W.stride(0), N, K, _ptr(perm), group, _ptr(Wq), _ptr(Sw), _stream(stream))
+    _check(fn, st)
     return Wq, Sw
 
 
+def comet_pack_weight_bf16s(W: torch.Tensor, perm: Optional[torch.Tensor] = None, group: int = BLOCK, stream=None):
+    """f4: as comet_pack_weight, with bf16 scales Sw16 [K/group x N] (the quantization scale)."""
+    return comet_pack_weight_f16s(W, perm, group, stream, bf16=True)
+
+
+def comet_w4ax_gemm_bf16s(Xq8, Xq4, Sx, bits, Wq, Sw16, group: int = BLOCK, out=None, workspace=None, stream=None):
+    """f4: comet_w4ax_gemm with bf16 weight scales."""
+    return comet_w4ax_gemm_f16s(Xq8, Xq4, Sx, bits, Wq, Sw16, group, out, workspace, stream)
+
+
 def comet_w4ax_gemm_f16s(Xq8, Xq4, Sx, bits, Wq, Sw16, group: int = BLOCK, out=None, workspace=None, stream=None):
-    """f4: comet_w4ax_gemm with fp16 weight scales."""
+    """f4: comet_w4ax_gemm with fp16 (or, for a bf16 Sw16, bf16) weight scales."""
     b = as_bits(bits)
     M = Xq8.shape[0] if b.n8 else Xq4.shape[0]
     N, K = Wq.shape[0], Wq.shape[1] * 2
@@ -345,10 +362,11 @@ def comet_w4ax_gemm_f16s(Xq8, Xq4, Sx, bits, Wq, Sw16, group: int = BLOCK, out=N
     need = int(lib().comet_w4ax_gemm_f16s_workspace_bytes(M, N, K, group))
     if workspace is None or workspace.numel() < need:
         workspace = new_workspace(need, Wq.device)
-    st = lib().comet_w4ax_gemm_f16s(_ptr(Xq8) if b.n8 else None, _ptr(Xq4) if b.n4 else None, _ptr(Sx), Sx.shape[1],
-                                    b.ptr, M, K, _ptr(Wq), _ptr(Sw16), N, group, _ptr(Y), Y.stride(0),
-                                    _ptr(workspace), workspace.numel(), _stream(stream))
-    _check("comet_w4ax_gemm_f16s", st)
+    fn = "comet_w4ax_gemm_bf16s" if Sw16.dtype == torch.bfloat16 else "comet_w4ax_gemm_f16s"
+    st = getattr(lib(), fn)(_ptr(Xq8) if b.n8 else None, _ptr(Xq4) if b.n4 else None, _ptr(Sx), Sx.shape[1],
+                            b.ptr, M, K, _ptr(Wq), _ptr(Sw16), N, group, _ptr(Y), Y.stride(0),
+                            _ptr(workspace), workspace.numel(), _stream(stream))
+    _check(fn, st)
     return Y
 
 

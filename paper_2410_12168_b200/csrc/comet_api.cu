@@ -881,9 +881,12 @@ comet_status comet_gather_shards(const void* Yall, int32_t P, int32_t M, int32_t
   return check_launch();
 }
 
-// ---- f4: FP16 weight-scale storage ---------------------------------------
-comet_status comet_pack_weight_f16s(const void* W, int64_t ldw, int32_t N, int32_t K, const int32_t* perm,
-                                    int32_t group, void* Wq, void* Sw16, comet_stream_t stream) {
+// ---- f4: FP16 / BF16 weight-scale storage ---------------------------------
+}  // extern "C"
+namespace {
+template <bool kBf16S>
+comet_status pack_weight_h16s(const void* W, int64_t ldw, int32_t N, int32_t K, const int32_t* perm, int32_t group,
+                              void* Wq, void* Sw16, comet_stream_t stream) {
   if (N < 0 || K <= 0) return COMET_ERR_INVALID_ARG;
   if (K % 128 || K > 65536 || N % 128 || (group != 128 && group != K) || ldw < K || ldw % 8) return COMET_ERR_SHAPE;
   if (N == 0) return COMET_OK;
@@ -897,24 +900,20 @@ comet_status comet_pack_weight_f16s(const void* W, int64_t ldw, int32_t N, int32
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const __half* Wh = reinterpret_cast<const __half*>(W);
   if (perm)
-    pack_weight_f16s_kernel<true><<<grid, 256, 0, st>>>(Wh, ldw, N, K, group, perm, reinterpret_cast<uint8_t*>(Wq),
-                                                         reinterpret_cast<__half*>(Sw16));
+    pack_weight_f16s_kernel<true, kBf16S><<<grid, 256, 0, st>>>(Wh, ldw, N, K, group, perm,
+                                                                 reinterpret_cast<uint8_t*>(Wq),
+                                                                 reinterpret_cast<uint16_t*>(Sw16));
   else
-    pack_weight_f16s_kernel<false><<<grid, 256, 0, st>>>(Wh, ldw, N, K, group, perm, reinterpret_cast<uint8_t*>(Wq),
-                                                          reinterpret_cast<__half*>(Sw16));
+    pack_weight_f16s_kernel<false, kBf16S><<<grid, 256, 0, st>>>(Wh, ldw, N, K, group, perm,
+                                                                  reinterpret_cast<uint8_t*>(Wq),
+                                                                  reinterpret_cast<uint16_t*>(Sw16));
   return check_launch();
 }
 
-int64_t comet_w4ax_gemm_f16s_workspace_bytes(int32_t M, int32_t N, int32_t K, int32_t group) {
-  const int64_t base = comet_w4ax_gemm_workspace_bytes(M, N, K);
-  if (base < 0 || group <= 0 || K % group) return -1;
-  return align256(std::max<int64_t>(base, kCounterBytes)) + align256((int64_t)(K / group) * N * 4);
-}
-
-comet_status comet_w4ax_gemm_f16s(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
-                                  const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq, const void* Sw16,
-                                  int32_t N, int32_t group, void* Y, int64_t ldy, void* workspace,
-                                  size_t workspace_bytes, comet_stream_t stream) {
+template <bool kBf16S>
+comet_status gemm_h16s(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx, const uint8_t* block_bits,
+                       int32_t M, int32_t K, const void* Wq, const void* Sw16, int32_t N, int32_t group, void* Y,
+                       int64_t ldy, void* workspace, size_t workspace_bytes, comet_stream_t stream) {
   if (M < 0 || N < 0 || K <= 0 || !block_bits) return COMET_ERR_INVALID_ARG;
   if (K % 128 || N % 128 || (group != 128 && group != K)) return COMET_ERR_SHAPE;
   if (M == 0 || N == 0) return COMET_OK;
@@ -934,14 +933,47 @@ comet_status comet_w4ax_gemm_f16s(const int8_t* Xq8, const void* Xq4, const floa
   int64_t grid = (n + 255) / 256;
   if (grid > (int64_t)num_sms * 8) grid = (int64_t)num_sms * 8;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  cudaError_t e = launch_pdl(widen_scales_kernel, dim3((unsigned)grid), dim3(256), 0, st,
-                             reinterpret_cast<const __half*>(Sw16), n, sw32);
+  cudaError_t e = launch_pdl(widen_scales_kernel<kBf16S>, dim3((unsigned)grid), dim3(256), 0, st,
+                             reinterpret_cast<const uint16_t*>(Sw16), n, sw32);
   if (e != cudaSuccess) return cuda_fail(e);
   comet_status ls = check_launch();
   if (ls != COMET_OK) return ls;
   return gemm_common(Xq8, Xq4, Sx, ldsx, block_bits, M, K, Wq, sw32, N, group, Y, ldy, nullptr, workspace,
                      (size_t)base, st);
 }
+}  // namespace
+extern "C" {
+
+comet_status comet_pack_weight_f16s(const void* W, int64_t ldw, int32_t N, int32_t K, const int32_t* perm,
+                                    int32_t group, void* Wq, void* Sw16, comet_stream_t stream) {
+  return pack_weight_h16s<false>(W, ldw, N, K, perm, group, Wq, Sw16, stream);
+}
+comet_status comet_pack_weight_bf16s(const void* W, int64_t ldw, int32_t N, int32_t K, const int32_t* perm,
+                                     int32_t group, void* Wq, void* Sw16, comet_stream_t stream) {
+  return pack_weight_h16s<true>(W, ldw, N, K, perm, group, Wq, Sw16, stream);
+}
+
+int64_t comet_w4ax_gemm_f16s_workspace_bytes(int32_t M, int32_t N, int32_t K, int32_t group) {
+  const int64_t base = comet_w4ax_gemm_workspace_bytes(M, N, K);
+  if (base < 0 || group <= 0 || K % group) return -1;
+  return align256(std::max<int64_t>(base, kCounterBytes)) + align256((int64_t)(K / group) * N * 4);
+}
+
+comet_status comet_w4ax_gemm_f16s(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
+                                  const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq, const void* Sw16,
+                                  int32_t N, int32_t group, void* Y, int64_t ldy, void* workspace,
+                                  size_t workspace_bytes, comet_stream_t stream) {
+  return gemm_h16s<false>(Xq8, Xq4, Sx, ldsx, block_bits, M, K, Wq, Sw16, N, group, Y, ldy, workspace,
+                          workspace_bytes, stream);
+}
+comet_status comet_w4ax_gemm_bf16s(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
+                                   const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq, const void* Sw16,
+                                   int32_t N, int32_t group, void* Y, int64_t ldy, void* workspace,
+                                   size_t workspace_bytes, comet_stream_t stream) {
+  return gemm_h16s<true>(Xq8, Xq4, Sx, ldsx, block_bits, M, K, Wq, Sw16, N, group, Y, ldy, workspace,
+                         workspace_bytes, stream);
+}
+
 
 int64_t comet_attention_kv4_workspace_bytes(int32_t T, int32_t H) {
   if (T <= 0 || H <= 0) return -1;

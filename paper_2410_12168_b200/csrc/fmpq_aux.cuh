@@ -8,6 +8,7 @@
 //       dequantization an attention kernel applies.
 // All HBM-bound streaming kernels (coalesced 16-byte / 4-byte accesses).
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <stdint.h>
 
@@ -341,10 +342,10 @@ __global__ void __launch_bounds__(256) quantize_act_static_kernel(const __half* 
 // w / s)), -7, 7) -- the scale the weights are quantized with is the stored
 // fp16 one.  Warp per (row, group) for g = 128 (lane = 4 channels), warp per
 // row for g = K; packed into the tiled layout like comet_pack_weight.
-template <bool kPerm>
+template <bool kPerm, bool kBf16S = false>
 __global__ void __launch_bounds__(256) pack_weight_f16s_kernel(const __half* __restrict__ W, int64_t ldw, int N, int K,
                                                                int group, const int32_t* __restrict__ perm,
-                                                               uint8_t* __restrict__ Wq, __half* __restrict__ Sw) {
+                                                               uint8_t* __restrict__ Wq, uint16_t* __restrict__ Sw) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ng = K / group;
   const int64_t item = (int64_t)blockIdx.x * 8 + warp;  // (row, group)
@@ -359,12 +360,22 @@ __global__ void __launch_bounds__(256) pack_weight_f16s_kernel(const __half* __r
   }
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, off));
-  __half sh = __float2half_rn(1.0f);
-  if (a != 0.0f) {
-    sh = __float2half_rn(__fdiv_rn(a, 7.0f));
-    if (__half2float(sh) == 0.0f) sh = __ushort_as_half((unsigned short)1);  // 2^-24
+  // the stored scale: fp16 (kBf16S false) or bf16 bits of RN(a / 7)
+  uint16_t sbits;
+  float sf;
+  if (kBf16S) {
+    const __nv_bfloat16 sb = __float2bfloat16_rn(a != 0.0f ? __fdiv_rn(a, 7.0f) : 1.0f);  // bf16 keeps fp32's range
+    sbits = __bfloat16_as_ushort(sb);
+    sf = __bfloat162float(sb);
+  } else {
+    __half sh = __float2half_rn(1.0f);
+    if (a != 0.0f) {
+      sh = __float2half_rn(__fdiv_rn(a, 7.0f));
+      if (__half2float(sh) == 0.0f) sh = __ushort_as_half((unsigned short)1);  // 2^-24
+    }
+    sbits = __half_as_ushort(sh);
+    sf = __half2float(sh);
   }
-  const float sf = __half2float(sh);
   // each lane packs whole 8-value words of the group: word w covers channels 8w .. 8w+7
   for (int w = lane; w < group / 8; w += 32) {
     int32_t q[8];
@@ -377,15 +388,16 @@ __global__ void __launch_bounds__(256) pack_weight_f16s_kernel(const __half* __r
     *reinterpret_cast<uint32_t*>(Wq + wq_tiled_offset(n, ((int64_t)j * group + 8 * w) / 2, K / 128)) =
         pack_int4_word(q);
   }
-  if (lane == 0) Sw[(int64_t)j * N + n] = sh;
+  if (lane == 0) Sw[(int64_t)j * N + n] = sbits;
 }
 
 // fp16 scales -> the fp32 scales the GEMM kernels read (per GEMM call, into the workspace)
-__global__ void __launch_bounds__(256) widen_scales_kernel(const __half* __restrict__ in, int64_t n,
+template <bool kBf16S>
+__global__ void __launch_bounds__(256) widen_scales_kernel(const uint16_t* __restrict__ in, int64_t n,
                                                            float* __restrict__ out) {
   grid_dep_launch();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = __half2float(in[i]);
+    out[i] = kBf16S ? __uint_as_float((uint32_t)in[i] << 16) : __half2float(__ushort_as_half(in[i]));
 }
 
 // ---- f3: dequant-in-attention over the KV4 cache (§3.2, §6.1) ----
