@@ -94,26 +94,31 @@ constexpr int kLaneSMax = COMET_LANE_SMAX;  // stages in the ring at most
 // 2 stages (two CTAs per SM up to K = 14336) against 512 lanes and 3 stages
 // (one CTA per SM): K = 4096 42.0 -> 38.9 us, K = 8192 64.5 -> 61.4 us,
 // K = 14336 equal, step 2.312 -> 2.284 ms.
+// Without a permutation (contiguous 16-byte loads, no table) one big CTA
+// per SM with 3 stages stays ahead: 16384 x 8192 65 vs 71 us, 8192 x 28672
+// 115-126 vs 128 us.
+constexpr int kLaneThreadsNoPerm = 512, kLaneSMaxNoPerm = 3;
 inline LanePlan lane_plan(int M, int K, bool perm) {
   LanePlan p;
   const int nb = K / 128;
   const int nsub = K / kLaneSub;
   if (nb <= 0 || nsub > kLaneRowMax) return p;
+  const int target = perm ? kLaneMaxThreads : kLaneThreadsNoPerm;
   int ncomp;
   if (nsub >= 32) {
     p.lpr = (nsub + 31) / 32 * 32;
-    p.R = std::max(1, kLaneMaxThreads / p.lpr);
+    p.R = std::max(1, target / p.lpr);
     ncomp = p.R * p.lpr;
   } else {
     p.lpr = nsub;
-    p.R = (kLaneMaxThreads / 32) * (32 / nsub);
-    ncomp = kLaneMaxThreads;
+    p.R = (target / 32) * (32 / nsub);
+    ncomp = target;
   }
   if (p.lpr > 32 && p.R > 15) return LanePlan{};  // named barriers 1..15
   p.threads = ncomp + 32;
   const int stage = p.R * K * 2;
   const int fixed = (perm ? K * 4 : 0) + ((2 * nb + 15) / 16) * 16 + 128;  // table + rho + barriers (2 x 8)
-  p.S = std::min(kLaneSMax, (kLaneMaxSmem - fixed) / stage);
+  p.S = std::min(perm ? kLaneSMax : kLaneSMaxNoPerm, (kLaneMaxSmem - fixed) / stage);
   if (p.S < 2) return LanePlan{};
   p.smem = p.S * stage + fixed;
   p.stages = ((int64_t)M + p.R - 1) / p.R;
