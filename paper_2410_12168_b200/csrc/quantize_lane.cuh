@@ -1,34 +1,36 @@
 // quantize_lane.cuh -- a1 + a2 (FMPQ activation quantize/pack with the fused
-// channel gather, P:L185 + P:L194 §3.2) for prefill-sized M: one THREAD per
-// (row, 128-channel block) item.
+// channel gather, P:L185 + P:L194 §3.2) for prefill-sized M (>= 512 rows):
+// one THREAD per 64 channels of a (row, 128-channel block) item.
 //
-// Why a thread per item: the half-warp-per-item kernels (quantize.cuh) spend
-// more instructions on the per-item shuffle trees (absmax, sum q), the scale
-// division and the per-element gather addressing than on the quantization
-// itself (~20 lane instructions per element, issue-bound at 2 TB/s with the
-// permutation).  Here a lane owns all 128 channels of its item: the absmax is
-// a register reduction, the scale pair is computed once per 128 elements and
-// nothing crosses lanes.
+// Why lanes own their channels: the half-warp-per-item kernels (quantize.cuh)
+// spend more instructions on the per-item shuffle trees (absmax, sum q), the
+// scale division and the per-element gather addressing than on the
+// quantization itself (~20 lane instructions per element, issue-bound at
+// 2 TB/s with the permutation).  Here a lane owns 64 channels of a block (its
+// partner lane the other 64): the absmax is a register reduction plus one
+// shuffle, the scale pair is computed once per 64 elements.
 //
-// Data flow (persistent CTAs, one per SM):
-//   * a stage = R consecutive rows (R * nb items = the compute threads, ~256);
-//     a producer warp brings each row in with one 1-D bulk copy into an S-deep
-//     ring of stages (mbarrier complete_tx);
-//   * gather: the lane reads its 128 source channels from the staged row with
+// Data flow (persistent CTAs, as many per SM as shared memory allows):
+//   * a stage = R consecutive rows (R * K / 64 sub-items = the compute lanes,
+//     ~256 with the permutation, ~512 without); a producer warp brings each
+//     row in with one 1-D bulk copy into an S-deep ring of stages (mbarrier
+//     complete_tx);
+//   * gather: the lane reads its 64 source channels from the staged row with
 //     2-byte shared loads at offsets from a per-CTA table built once from the
-//     permutation (identity without one);
-//   * bank conflicts: lanes of a warp hold consecutive blocks, whose source
-//     positions (for the mostly monotone FMPQ permutation: outliers first, the
-//     rest in order) are 256 B apart -- the same bank.  Each block's walk is
-//     therefore ROTATED by rho_b (even) so that lane b starts on bank b mod
-//     32: step j reads position (j + rho_b) mod 128, which for a monotone run
-//     lands on bank (b + j/2) mod 32, distinct across the warp.  The table
-//     stores the offsets in walk order (u32, per block 32 chunks of 4, XOR-
-//     swizzled for conflict-free 16-byte reads);
-//   * after all lanes of the CTA finished gathering (named barrier), each lane
-//     quantizes and writes its 128 output bytes back IN PLACE into its row's
-//     staging slot (INT4 plane part first, then the INT8 part), undoing the
-//     rotation with one byte-permute per word and a rotated word address;
+//     permutation; without one, rotated 16-byte loads of the contiguous run;
+//   * bank conflicts: lanes of a warp hold consecutive sub-blocks, whose
+//     source positions (for the mostly monotone FMPQ permutation: outliers
+//     first, the rest in order) are 128 B apart -- the same bank.  Each
+//     sub-block's walk is therefore ROTATED by rho_c (even) so that lane c
+//     starts on bank c mod 32: step j reads position (j + rho_c) mod 64, which
+//     for a monotone run lands on bank (c + j/2) mod 32.  The table stores the
+//     offsets in walk order (u32, per sub-block 16 chunks of 4, XOR-swizzled
+//     for conflict-free 16-byte reads);
+//   * after all lanes of a ROW finished gathering (named barrier per row),
+//     each lane quantizes and writes its 64 output bytes back IN PLACE into
+//     its row's staging slot (INT4 plane part first, then the INT8 part),
+//     undoing the rotation with one byte-permute per word and a rotated word
+//     address;
 //   * the producer bulk-stores each row's plane segments to global memory and
 //     refills the slot once the store has read it.
 // Output is bit-identical to quantize_act_kernel / quantize_act_rows_kernel
