@@ -518,10 +518,10 @@ comet_status quantize_act_impl(const void* X, int64_t ldx, int32_t M, int32_t K,
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, lp.threads, lp.smem);
       if (e != cudaSuccess) return cuda_fail(e);
       const int64_t grid = std::min<int64_t>((int64_t)num_sms * std::max(1, per_sm), lp.stages);
-      kern<<<(int)grid, lp.threads, lp.smem, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
-                                                    X4e ? X4e : reinterpret_cast<uint8_t*>(Xq4),
-                                                    X4e ? (int64_t)n4 * 128 : (int64_t)n4 * 64, Sx, CX, lp.R, lp.S,
-                                                    lp.lpr);
+      e = launch_pdl(kern, dim3((unsigned)grid), dim3(lp.threads), lp.smem, st, Xh, ldx, M, K / 128, ldsx, perm,
+                     map, Xq8, (int64_t)n8 * 128, X4e ? X4e : reinterpret_cast<uint8_t*>(Xq4),
+                     X4e ? (int64_t)n4 * 128 : (int64_t)n4 * 64, Sx, CX, lp.R, lp.S, lp.lpr);
+      if (e != cudaSuccess) return cuda_fail(e);
       return check_launch();
     }
   }
@@ -546,21 +546,20 @@ comet_status quantize_act_impl(const void* X, int64_t ldx, int32_t M, int32_t K,
       if (per_sm < 1) per_sm = 1;
       int64_t grid = (int64_t)num_sms * per_sm;
       if (grid > ldsx) grid = ldsx;
-      kern<<<(int)grid, kQThreads, smem, st>>>(Xh, ldx, M, K / 128, ldsx, pk, map, Xq8, (int64_t)n8 * 128,
-                                         X4e ? X4e : reinterpret_cast<uint8_t*>(Xq4),
-                                         X4e ? (int64_t)n4 * 128 : (int64_t)n4 * 64, Sx, nullptr, CX);
+      e = launch_pdl(kern, dim3((unsigned)grid), dim3(kQThreads), smem, st, Xh, ldx, M, K / 128, ldsx, pk, map, Xq8,
+                     (int64_t)n8 * 128, X4e ? X4e : reinterpret_cast<uint8_t*>(Xq4),
+                     X4e ? (int64_t)n4 * 128 : (int64_t)n4 * 64, Sx, static_cast<const float*>(nullptr), CX);
+      if (e != cudaSuccess) return cuda_fail(e);
       return check_launch();
     }
   }
   if (X4e) return COMET_ERR_UNSUPPORTED;  // the fused output needs the row-staged kernel
   // one CTA per (8 rows, 2 blocks): 16 half-warp items
   const dim3 grid((unsigned)((ldsx + 7) / 8), (unsigned)((K / 128 + 1) / 2));
-  if (perm)
-    quantize_act_kernel<true, false, kBf16><<<grid, 256, 0, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
-                                                          reinterpret_cast<uint8_t*>(Xq4), (int64_t)n4 * 64, Sx);
-  else
-    quantize_act_kernel<false, false, kBf16><<<grid, 256, 0, st>>>(Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
-                                                           reinterpret_cast<uint8_t*>(Xq4), (int64_t)n4 * 64, Sx);
+  cudaError_t e = launch_pdl(perm ? quantize_act_kernel<true, false, kBf16> : quantize_act_kernel<false, false, kBf16>,
+                             grid, dim3(256), 0, st, Xh, ldx, M, K / 128, ldsx, perm, map, Xq8, (int64_t)n8 * 128,
+                             reinterpret_cast<uint8_t*>(Xq4), (int64_t)n4 * 64, Sx);
+  if (e != cudaSuccess) return cuda_fail(e);
   return check_launch();
 }
 

@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(256) quantize_act_static_kernel(const __half* 
                                                                   int8_t* __restrict__ Xq8, int64_t ld8,
                                                                   uint8_t* __restrict__ Xq4, int64_t ld4,
                                                                   float* __restrict__ Sx) {
+  grid_dep_wait();  // (no-op unless PDL-launched behind a kernel that reads this call's outputs)
   grid_dep_launch();
   const int half_id = threadIdx.x >> 4;
   const int o = threadIdx.x & 15;
@@ -395,6 +396,7 @@ __global__ void __launch_bounds__(256) pack_weight_f16s_kernel(const __half* __r
 template <bool kBf16S>
 __global__ void __launch_bounds__(256) widen_scales_kernel(const uint16_t* __restrict__ in, int64_t n,
                                                            float* __restrict__ out) {
+  grid_dep_wait();  // PDL: a preceding GEMM on the same workspace may still read the widened scales
   grid_dep_launch();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = kBf16S ? __uint_as_float((uint32_t)in[i] << 16) : __half2float(__ushort_as_half(in[i]));

@@ -212,6 +212,8 @@ __global__ void __launch_bounds__(DEC_LB > 0 ? DEC_LB : DecCfg<BN>::kThreads, 1)
   if (warp == C::kMmaWarp) tmem_alloc<C::kTmemCols>(tmem_holder);
   tc_fence_before();
   __syncthreads();
+  // (no griddepcontrol.launch_dependents here: letting the next layer's
+  // quantizer launch early slowed the 70B decode step 0.137 -> 0.158 ms)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 

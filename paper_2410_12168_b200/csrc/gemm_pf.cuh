@@ -289,6 +289,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PF_LB > 0 ? PF_LB : 
   __syncthreads();  // orders the allocation's smem write before the reads below for racecheck (cluster_sync does in hardware)
   cluster_sync();
   tc_fence_after();
+  // PDL: the next kernel in the stream (e.g. the next layer's quantizer) may
+  // be scheduled; its CTAs take SMs as this grid's CTAs exit and wait for
+  // this grid's completion before touching memory (griddepcontrol.wait)
+  grid_dep_launch();
   const uint32_t tmem_base = *tmem_holder;
   // debug trace of one CTA (-DCOMET_TRACE builds only; tools/gemm_sweep.py trace_pf)
   const bool tr = kTraceBuild && g_cta_times_on && blockIdx.x + 1 == g_cta_times_on;

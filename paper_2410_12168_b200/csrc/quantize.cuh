@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(256) quantize_act_kernel(const __half* __restr
                                                            const __grid_constant__ BlockMap map, int8_t* __restrict__ Xq8,
                                                            int64_t ld8, uint8_t* __restrict__ Xq4, int64_t ld4,
                                                            float* __restrict__ Sx) {
+  grid_dep_wait();    // PDL launch: the preceding kernel (which may read this call's outputs) is complete
   grid_dep_launch();  // the GEMM that follows may get scheduled (PDL)
   const int half_id = threadIdx.x >> 4;  // 16 half-warps per CTA
   const int o = threadIdx.x & 15;        // octet within the block
@@ -446,6 +447,7 @@ __global__ void __launch_bounds__(kQThreads, COMET_Q_MINB) quantize_act_rows_ker
                                                                 const float* __restrict__ sstat = nullptr,
                                                                 float* __restrict__ CX = nullptr) {
   extern __shared__ __align__(16) uint8_t qsm[];
+  grid_dep_wait();    // PDL launch: the preceding kernel (which may read this call's outputs) is complete
   grid_dep_launch();  // the GEMM that follows may get scheduled (PDL)
   const int K = nb * 128;
   __shared__ uint64_t rbar[kQNBuf];

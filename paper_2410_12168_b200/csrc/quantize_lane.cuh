@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(kE4 ? COMET_LANE_LB_E4 : COMET_LANE_LB_PK, 1)
   constexpr int kW = kSub / 2;       // packed pairs per lane
   constexpr int kSpb = 128 / kSub;   // lanes per 128-channel block
   extern __shared__ __align__(128) uint8_t lsm[];
+  grid_dep_wait();    // PDL launch: the preceding kernel (which may read this call's outputs) is complete
   grid_dep_launch();  // the GEMM that follows may get scheduled (PDL)
   const int K = nb * 128;
   const int nsub = nb * kSpb;
