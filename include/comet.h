@@ -123,7 +123,15 @@ comet_status comet_quantize_act_bf16(const void* X, int64_t ldx, int32_t M, int3
  * fp16.  N % 128 == 0.  workspace: device memory of at least
  * comet_w4ax_gemm_workspace_bytes(M, N, K) bytes (16-byte aligned) whose first 64 KiB must be
  * zero on the first use (the kernel leaves it zero again); it may be NULL
- * only if that size is 0. */
+ * only if that size is 0.
+ * Stream ordering: every library kernel is launched with programmatic stream
+ * serialization and executes griddepcontrol.wait before touching memory a
+ * preceding kernel may use; the prefill GEMM (M > 128, or M > 64 with
+ * per-channel scales) signals griddepcontrol.launch_dependents after its
+ * prologue, so a CALLER kernel launched right after it with programmatic
+ * stream serialization must itself wait (griddepcontrol.wait /
+ * cudaGridDependencySynchronize) before reading Y.  Ordinary launches,
+ * events and copies are unaffected. */
 comet_status comet_w4ax_gemm(const int8_t* Xq8, const void* Xq4, const float* Sx, int64_t ldsx,
                              const uint8_t* block_bits, int32_t M, int32_t K, const void* Wq, const float* Sw,
                              int32_t N, int32_t group, void* Y, int64_t ldy, void* workspace,
