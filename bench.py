@@ -155,9 +155,21 @@ class ClockSampler:
 
 
 # ------------------------------------------------------ distributed ----
+# tools only: COMET_BENCH_FORCE_TP=1 under a 1-rank torchrun runs the N > 1
+# exchange path (process group, symmetric-memory outputs, fused all-gather
+# epilogue, barriers) on one GPU, to check its plumbing where no second GPU exists
+FORCE_TP = os.environ.get("COMET_BENCH_FORCE_TP") == "1"
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1:
+    if world > 1 or (FORCE_TP and "RANK" in os.environ):
+        # stdout carries exactly one JSON line: NCCL's log lines go to stderr,
+        # and NCCL_DEBUG=VERSION (set in this image), whose "NCCL version"
+        # banner is printed to stdout regardless, is lowered to WARN
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "WARN"
         import torch
         import torch.distributed as dist
         rank, local = int(os.environ["RANK"]), int(os.environ.get("LOCAL_RANK", "0"))
@@ -309,7 +321,7 @@ def run_comet(args, cfg, config_name):
     # full output (symmetric memory, NVLink P2P) and one barrier ends the layer; fallback (no
     # symmetric memory): row chunks pipelining GEMM and an NCCL all-gather
     exchange = "single"
-    if world > 1:
+    if world > 1 or FORCE_TP:
         exchange = "nccl"
         if args.tp_exchange == "fused":
             try:
@@ -371,7 +383,7 @@ def run_comet(args, cfg, config_name):
             dist.barrier()
         torch.cuda.synchronize()
 
-    use_graph = world == 1
+    use_graph = world == 1 and exchange == "single"
     preroll = M <= 256 and not use_graph
 
     def time_steps(gname, nsteps, nwarm):
@@ -539,7 +551,7 @@ def run_comet(args, cfg, config_name):
         out["cpu_baseline"] = cpu_baseline(cfg, args, seconds_target=args.cpu_seconds)
     if rank == 0:
         print(json.dumps(out))
-    if world > 1:
+    if world > 1 or (FORCE_TP and dist.is_initialized()):
         dist.barrier()
         dist.destroy_process_group()
     return 0
