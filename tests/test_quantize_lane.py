@@ -84,3 +84,35 @@ def test_lane_quantizer_e4_linear_matches_two_call_path(M, K, n8, kind):
     Y = comet.comet_w4ax_linear(X, bits, Wq, Sw, perm=perm, group=128, scratch=scratch)
     torch.cuda.synchronize()
     assert np.array_equal(Y.cpu().numpy().view(np.uint16), ref.cpu().numpy().view(np.uint16))
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_lane_quantizer_random_configs(seed):
+    """Random shapes, masks and permutations (M >= 512, K up to 28672): planes
+    and Sx bit-exact; the e4m3 linear path identical to the two-call path."""
+    rng = np.random.default_rng(1000 + seed)
+    nb = int(rng.choice([1, 3, 8, 31, 32, 33, 64, 86, 112, 150, 224]))
+    K = 128 * nb
+    M = int(rng.integers(512, 2600))
+    n8 = int(rng.integers(0, max(1, nb // 3) + 1))
+    mask = str(rng.choice(["prefix", "scattered"]))
+    kind = str(rng.choice(["fmpq", "random", "none"]))
+    p = make(M, K, n8, kind, seed=seed, mask=mask)
+    bits = comet.BlockBits(p["bits"])
+    X, perm = to_dev(p["X"]), to_dev(p["perm"])
+    g8, g4, gs = comet.comet_quantize_act(X, bits, perm)
+    torch.cuda.synchronize()
+    o8, o4, os_ = oracle.quantize_act(p["X"], p["bits"], p["perm"])
+    assert np.array_equal(g8.cpu().numpy().view(np.uint8), o8.view(np.uint8))
+    assert np.array_equal(g4.cpu().numpy().view(np.uint8), o4.view(np.uint8))
+    assert np.array_equal(gs.cpu().numpy().view(np.uint32), os_.view(np.uint32))
+    if K <= 8192:
+        N = 384
+        W = to_dev((rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float16))
+        Wq, Sw = comet.comet_pack_weight(W, perm, K)
+        ws = comet.new_workspace(comet.comet_w4ax_gemm_workspace_bytes(M, N, K), X.device)
+        ref = comet.comet_w4ax_gemm(g8, g4, gs, bits, Wq, Sw, K, workspace=ws)
+        scratch = comet.new_workspace(comet.comet_w4ax_linear_scratch_bytes(M, N, K, bits), X.device)
+        Y = comet.comet_w4ax_linear(X, bits, Wq, Sw, perm=perm, group=K, scratch=scratch)
+        torch.cuda.synchronize()
+        assert np.array_equal(Y.cpu().numpy().view(np.uint16), ref.cpu().numpy().view(np.uint16))
